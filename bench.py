@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the temporally-blocked fp64 stencil sweep (BASELINE.json metric: MLUP/s).
+
+Default workload = BASELINE.json configs[1]: var7pt, 512^3 interior, 1-cell Dirichlet halo,
+7 coefficient grids in [0, 0.14), field in [0, 1), 100 time steps, seed 42 (synthetic inputs
+generated on the device with the reference's counter-based generator + SURVEY.md 8(d) remap).
+One bench "step" = one girih_gpu_step(100) call = the full 100-time-step sweep of the config.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--stencil var7pt --n 512]
+
+Prints ONE JSON line (rank 0). `value` is device-timed MLUP/s with inputs resident in HBM;
+`e2e` is the same metric through the drop-in C-ABI call girih_gpu_run on pinned host buffers
+(H2D of u, v, coefficients + D2H of u, v inside the timed region). `--impl reference` times the
+reference's own CPU engine (girih::run, MWD, all host cores) from oracle/_ref.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KINDS = ("const7pt", "var7pt", "const25pt", "var25pt")
+B1 = {0: 16, 1: 72, 2: 32, 3: 120}          # compulsory bytes/LUP of one sweep
+DP_OPS = {0: 10, 1: 13, 2: 33, 3: 37}       # DMUL+DADD per LUP in the reference association
+FLOPS = {0: 7, 1: 13, 2: 33, 3: 37}         # traits flops/LUP (stencil.cpp:11-17)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic(kind: int, n: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"{KINDS[kind]}_{n}")
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), e.get("source")
+
+
+# ------------------------------------------------------------------------------------------
+# CPU arms: the reference's own engine (oracle/_ref) -- checker/baseline only
+# ------------------------------------------------------------------------------------------
+def cpu_reference_sample(kind: int, n: int, target_s: float, max_steps: int, reps: int = 1):
+    """Times girih::run (MWD, engine.cpp:332-418) on all host threads on a bounded sample of the
+    workload (same grid, fewer steps). Returns dict with MLUP/s and what was sampled."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import Oracle, RefLib, RefState
+
+    lib, orc = RefLib(), Oracle()
+    threads = os.cpu_count() or 1
+    R = 1 if kind < 2 else 4
+    dw = 8 if R == 1 else 16
+    variant = 0 if R == 1 else 1  # relaxed for 7-pt, FED for 25-pt
+    st = RefState(lib, kind, n, n, n, 0, 42, oracle_fill=orc, remap=True)
+    # calibrate on one diamond height, then size the sample to ~target_s
+    cal = max(1, dw // (2 * R))
+    wall, _ = st.run(cal, dw, 4, (1, 1, 1), variant, threads)
+    rate = n ** 3 * cal / max(wall, 1e-9)
+    steps = int(max(1, min(max_steps, target_s * rate / n ** 3)))
+    best = None
+    results = []
+    for _ in range(reps):
+        wall, _ = st.run(steps, dw, 4, (1, 1, 1), variant, threads)
+        results.append(wall)
+        best = wall if best is None else min(best, wall)
+    mlups = n ** 3 * steps / best / 1e6
+    return dict(value=mlups, unit="MLUP/s", cores=threads, kind="reference",
+                sample=f"girih::run MWD {KINDS[kind]} {n}^3, {steps} steps (of 100), dw={dw}, "
+                       f"nf=4, {'relaxed' if variant == 0 else 'fed'}, {threads} groups x 1x1x1, "
+                       f"best of {reps}", walls=results, steps=steps)
+
+
+def run_reference_arm(args, rank: int):
+    if rank != 0:
+        return 0
+    kind = KINDS.index(args.stencil)
+    n = args.n
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import Oracle, RefLib, RefState
+
+    lib, orc = RefLib(), Oracle()
+    threads = os.cpu_count() or 1
+    R = 1 if kind < 2 else 4
+    dw = 8 if R == 1 else 16
+    variant = 0 if R == 1 else 1
+    st = RefState(lib, kind, n, n, n, 0, 42, oracle_fill=orc, remap=True)
+    cal = max(1, dw // (2 * R))
+    wall, _ = st.run(cal, dw, 4, (1, 1, 1), variant, threads)
+    rate = n ** 3 * cal / max(wall, 1e-9)
+    # each step: a bounded sample so that (warmup + steps) samples take ~ budget_s
+    per = args.ref_budget_s / max(1, args.steps + args.warmup)
+    steps_per = int(max(1, min(100, per * rate / n ** 3)))
+    for _ in range(args.warmup):
+        st.run(steps_per, dw, 4, (1, 1, 1), variant, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st.run(steps_per, dw, 4, (1, 1, 1), variant, threads)
+    dt = time.perf_counter() - t0
+    lups = n ** 3 * steps_per * args.steps
+    value = lups / dt / 1e6
+    line = {
+        "impl": "reference", "metric": f"fp64 MLUP/s ({KINDS[kind]} {n}^3)", "value": value,
+        "unit": "MLUP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded init_state + remap)",
+        "config": {"workload": f"{KINDS[kind]} {n}^3 interior, seed 42, bounded sample of "
+                               f"{steps_per} of 100 time steps per step"},
+        "cpu_baseline": {"value": value, "unit": "MLUP/s", "cores": threads, "kind": "reference",
+                         "sample": f"girih::run MWD {KINDS[kind]} {n}^3 x {steps_per} steps per "
+                                   f"bench step, dw={dw}, nf=4, {threads} groups"},
+        "e2e": {"value": value, "unit": "MLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def run_gpu_arm(args, rank: int, world: int, local_rank: int):
+    import paper_1510_04995_b200 as g
+
+    kind = KINDS.index(args.stencil)
+    n = args.n
+    T = args.nt
+    dev = local_rank
+    hbm, hbm_src = measured_peaks()
+    grid = g.GridSpec(n, n, n, 0)
+    cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant)
+    if world > 1:
+        raise SystemExit("multi-rank bench path: see run_gpu_multirank")
+    ds = g.DeviceState.seeded(kind, grid, 42, remap=True, config=cfg)
+    tuned = None
+    if args.tune:
+        tcfg, tml, nmeas = ds.tune(max_tb=args.tb if args.tb > 0 else 0)
+        tcfg.device = dev
+        ds.set_config(tcfg)
+        tuned = {"tb": tcfg.tb, "variant": tcfg.variant, "zchunks": tcfg.zchunks,
+                 "mlups": tml, "measured": nmeas}
+    for _ in range(args.warmup):
+        ds.step(T)
+    reps = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            reps.append(ds.step(T))
+    kernel_s = sum(r.kernel_seconds for r in reps)
+    lups = sum(r.lups for r in reps)
+    value = lups / kernel_s / 1e6
+    launches = sum(r.n_launches for r in reps)
+    pass_s = sum(r.pass_seconds for r in reps)
+    avg_launch = pass_s / max(1, launches)
+    cells = n ** 3
+    achieved = cells * B1[kind] / avg_launch / 1e9  # algorithmic bytes per launch / duration
+    traffic, traffic_src = ncu_traffic(kind, n)
+    r0 = reps[-1]
+    ds.close()
+
+    # ---- e2e: the drop-in C-ABI call on pinned host buffers (H2D + sweep + D2H timed) ----
+    e2e = None
+    if not args.no_e2e:
+        with g.DeviceState.seeded(kind, grid, 42, remap=True, config=cfg) as ds2:
+            host = ds2.download(pinned=True)
+        e2e_cfg = g.GpuConfig(tb=r0.tb_used, variant=r0.variant_used, zchunks=args.zchunks,
+                              device=dev)
+        walls, h2d, d2h = [], 0, 0
+        for rep in range(args.e2e_steps + 1):
+            host.t_current = 0
+            pr = g.run(host, T, e2e_cfg)
+            if rep > 0:  # first call is the warm-up
+                walls.append(pr.wall_seconds)
+                h2d, d2h = pr.h2d_bytes, pr.d2h_bytes
+        e2e = {"value": cells * T / (sum(walls) / len(walls)) / 1e6, "unit": "MLUP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": sum(walls) / len(walls) * 1e3}
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_reference_sample(kind, n, args.cpu_target_s, 100)
+        cpu.pop("walls", None)
+        cpu.pop("steps", None)
+
+    fp64 = None
+    try:
+        addmul, dfma = g.fp64_peak(dev)
+        ops = DP_OPS[kind] * r0.computed_lups / max(r0.pass_seconds, 1e-12)
+        fp64 = {"dp_ops_per_s_achieved": ops, "dp_ops_per_s_peak_measured": addmul,
+                "frac": ops / addmul, "dfma_flops_peak_measured": dfma,
+                "redundancy": r0.computed_lups / r0.lups}
+    except Exception as e:  # noqa: BLE001
+        fp64 = {"error": str(e)}
+
+    line = {
+        "metric": f"fp64 MLUP/s ({KINDS[kind]} {n}^3, {T} steps)",
+        "value": value, "unit": "MLUP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": kernel_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: device-generated init_state(seed 42) + SURVEY 8(d) remap",
+        "config": {"workload": f"BASELINE configs[1]: {KINDS[kind]} {n}^3 interior, T={T}, "
+                               f"seed 42", "stencil": KINDS[kind], "n": n, "time_steps": T,
+                   "tb": r0.tb_used, "variant": r0.variant_used, "zchunks": r0.zchunks_used,
+                   "grid_ctas": r0.grid_ctas, "passes_per_step": r0.n_launches,
+                   "l2": f"inputs {cells * 8 * (2 + (7 if kind == 1 else 13 if kind == 3 else kind // 2)) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                   "tuned": tuned},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "peak_source": hbm_src, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": cells * B1[kind],
+                     "avg_launch_ms": avg_launch * 1e3,
+                     "lup_roofline_mlups": hbm * 1e9 * r0.tb_used / B1[kind] / 1e6,
+                     "frac_of_lup_roofline": value / (hbm * 1e9 * r0.tb_used / B1[kind] / 1e6),
+                     "frac_of_tb1_roofline": value / (hbm * 1e9 / B1[kind] / 1e6)},
+        "fp64": fp64,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="girih", choices=["girih", "reference"])
+    ap.add_argument("--stencil", default="var7pt", choices=KINDS)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--nt", type=int, default=100)
+    ap.add_argument("--tb", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=-1)
+    ap.add_argument("--zchunks", type=int, default=0)
+    ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-target-s", type=float, default=10.0)
+    ap.add_argument("--ref-budget-s", type=float, default=120.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference_arm(args, rank)
+    return run_gpu_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

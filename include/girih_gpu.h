@@ -1,0 +1,167 @@
+/* girih_gpu.h -- C ABI of the B200-native temporally-blocked fp64 stencil sweep.
+ *
+ * Drop-in boundary for the reference's hot path
+ *     girih::run(ProblemState&, long steps, int dw, const WavefrontSpec&,
+ *                const ThreadGroupShape&, WavefrontVariant, int n_groups, const RunOptions&)
+ * declared at /root/reference/proj/include/girih/engine.hpp:111-115 and implemented at
+ * proj/src/engine.cpp:332-418. The reference's callers (verify_once, proj/tools/main.cpp:136;
+ * cmd_run, main.cpp:295; make_engine_measure, proj/src/tuner.cpp:220) reach this ABI through
+ * the header-only C++ shim include/girih_gpu.hpp (girih::gpu::run), see INTEGRATION.md.
+ *
+ * Plain pointers and sizes only. Every function returns an int status:
+ *   GIRIH_OK (0); GIRIH_EINVAL (-1) <-> std::invalid_argument in the reference
+ *   (negative steps, bad kind, extent < 2R+1, negative padding, bad config);
+ *   GIRIH_ECUDA / GIRIH_ENCCL / GIRIH_ENOMEM <-> std::runtime_error;
+ *   GIRIH_ESTATE <-> std::logic_error (handle misuse).
+ * girih_gpu_last_error() returns a thread-local message for the last failure.
+ *
+ * Host arrays use the reference layout (proj/include/girih/stencil.hpp:31-73): dense
+ * [k][j][i] doubles, X = nx + 2R + pad_x, Y = ny + 2R, Z = nz + 2R. Level parity follows
+ * stencil.hpp:78-98: time level t lives in u when t is even, in v when t is odd; after a
+ * run of T >= 1 steps from t0, the field of parity(t0+T) holds level t0+T and the other
+ * field holds level t0+T-1; ghost and pad cells are never written.
+ */
+#ifndef GIRIH_GPU_H
+#define GIRIH_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIRIH_GPU_ABI_VERSION 1
+
+#define GIRIH_OK 0
+#define GIRIH_EINVAL (-1)
+#define GIRIH_ECUDA (-2)
+#define GIRIH_ENCCL (-3)
+#define GIRIH_ENOMEM (-4)
+#define GIRIH_ESTATE (-5)
+
+/* girih::StencilKind order (stencil.hpp:15) */
+#define GIRIH_CONST7PT 0
+#define GIRIH_VAR7PT 1
+#define GIRIH_CONST25PT 2
+#define GIRIH_VAR25PT 3
+
+/* Non-owning view of a host girih::ProblemState (stencil.hpp:83-98). */
+typedef struct {
+    int kind;
+    int nx, ny, nz, pad_x;
+    long long t_current;
+    double* u;                     /* even time levels */
+    double* v;                     /* odd time levels (level -1 seed for const25pt) */
+    const double* const* coeffs;   /* n_coeffs coefficient fields (0/7/1/13 by kind) */
+    int n_coeffs;
+    double cc[5];                  /* scalar coefficients c0..c4 */
+} girih_state_view;
+
+/* GPU execution parameters; they replace the CPU engine's (dw, wf, shape, variant, n_groups). */
+typedef struct {
+    int tb;        /* time steps fused per HBM pass; 0 = tuned/default for the kind */
+    int variant;   /* kernel tile variant index (see girih_gpu_variant_info); -1 = default */
+    int zchunks;   /* z chunks per tile column; 0 = auto (wave-quantisation model) */
+    int ngpus;     /* >1: z-slab decomposition over devices [device, device+ngpus) */
+    int exact;     /* 1 = bitwise mode (no FMA contraction); 0 is rejected */
+    int device;    /* CUDA device ordinal of the (first) GPU */
+    int graphs;    /* 1 = capture the pass sequence of a step call in a CUDA graph */
+    int reserved;
+} girih_gpu_config;
+
+typedef struct {
+    double wall_s;          /* host wall time of the call */
+    double kernel_s;        /* CUDA-event time of all device work of the step(s) */
+    double h2d_s, d2h_s;    /* copy times (girih_gpu_run only) */
+    long long lups;         /* nx*ny*nz*steps, interior only (engine.cpp:340) */
+    double mlups;           /* lups / kernel_s / 1e6 (girih_gpu_run: lups / wall_s / 1e6) */
+    double model_bytes_per_lup; /* algorithmic code balance B1/Tb of the plan */
+    int tb_used;            /* largest fused step count of the plan */
+    int n_launches;         /* stencil-pass kernel launches */
+    double pass_s;          /* summed CUDA-event durations of the stencil-pass launches */
+    long long computed_lups;/* LUPs evaluated incl. redundant halo recompute */
+    long long h2d_bytes, d2h_bytes;
+    int variant_used;
+    int zchunks_used;
+    int grid_ctas;
+    int reserved;
+} girih_gpu_report;
+
+/* kernel variant description (compiled tile shapes) */
+typedef struct {
+    int kind, tb, lx, ly, threads, prefetch;
+    int smem_bytes;
+} girih_gpu_variant;
+
+const char* girih_gpu_last_error(void);
+int girih_gpu_abi_version(void);
+
+/* traits() / stencil_from_name() (proj/src/stencil.cpp:11-17, 41-47) */
+int girih_gpu_traits(int kind, int* radius, int* domain_streams, int* flops_per_lup,
+                     int* time_order, int* coeff_arrays);
+int girih_gpu_kind_from_name(const char* name, int* kind);
+
+/* compiled kernel variants */
+int girih_gpu_variant_count(void);
+int girih_gpu_variant_info(int index, girih_gpu_variant* out);
+
+/* Open a device-resident state: allocates device buffers and uploads the host view. */
+int girih_gpu_open(const girih_state_view* state, const girih_gpu_config* cfg, void** handle);
+
+/* Open a device-resident state initialised ON THE DEVICE with the reference's
+ * counter-based generator (init_state, proj/src/stencil.cpp:58-85; values bit-identical).
+ * remap = 1 applies the BASELINE.json input remap. */
+int girih_gpu_open_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned long long seed,
+                          int remap, const girih_gpu_config* cfg, void** handle);
+
+/* Re-upload u, v, coefficients, cc and t_current from a host view of the same shape. */
+int girih_gpu_upload(void* handle, const girih_state_view* state);
+
+/* Advance the device state by `steps` (the timed, device-resident hot path). */
+int girih_gpu_step(void* handle, long long steps, girih_gpu_report* report);
+
+/* Download u, v and t_current into the view (u/v may be NULL to skip). */
+int girih_gpu_download(void* handle, girih_state_view* state);
+
+/* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
+int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double* cc);
+
+int girih_gpu_get_t(void* handle, long long* t_current);
+int girih_gpu_set_config(void* handle, const girih_gpu_config* cfg);
+int girih_gpu_close(void* handle);
+
+/* open + step + download + close: the drop-in for girih::run (engine.hpp:113-115). */
+int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
+                  girih_gpu_report* report);
+
+/* Host-side pass planner (exposed for tests): splits `steps` into passes of at most tb
+ * fused steps and assigns buffers. Buffer ids: 0 = u, 1 = v, 2 = even scratch,
+ * 3 = odd scratch; -1 = none. Arrays have room for max_passes entries. */
+int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_passes,
+                   int* n_passes, int* pass_tb, int* pass_src, int* pass_src_prev,
+                   int* pass_dst, int* pass_dst_penult);
+
+/* On-device auto-tuner (replaces girih::tune, proj/src/tuner.cpp:146-210): hill-climbs
+ * (tb, variant, zchunks) with CUDA-event timing and adaptive test sizing on the handle's
+ * own state (the state is restored afterwards). Writes the best config into *best. */
+int girih_gpu_tune(void* handle, int max_tb, girih_gpu_config* best, double* best_mlups,
+                   int* n_measured);
+
+/* pinned host memory helpers (for H2D/D2H at full PCIe rate) */
+int girih_gpu_host_alloc(size_t bytes, void** ptr);
+int girih_gpu_host_free(void* ptr);
+
+/* interior_checksum (proj/src/stencil.cpp:129-146) of the current level of a host view */
+int girih_gpu_interior_checksum(const girih_state_view* state, unsigned long long* out);
+
+/* measured FP64 rates on `device` (ops/s of separate DADD/DMUL and of DFMA) */
+int girih_gpu_fp64_peak(int device, double* dadd_dmul_ops_per_s, double* dfma_flops_per_s);
+
+/* device properties (SM count, name) */
+int girih_gpu_device_info(int device, int* sm_count, char* name, int name_len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GIRIH_GPU_H */

@@ -1,0 +1,17 @@
+// device_api.h -- host-callable launchers for the helper kernels (init_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace girih_gpu {
+
+cudaError_t launch_init_field(double* buf, int pitch, int off, int X, int Y, int Zloc, int zoff,
+                              int Zg, uint64_t seed, int field, int remap, double scale,
+                              cudaStream_t stream);
+
+// mode 0: separate DMUL+DADD chains (2 ops per step), mode 1: DFMA chains (2 flops per step)
+cudaError_t launch_fp64_probe(int mode, double* out, int blocks, int threads, int iters,
+                              cudaStream_t stream);
+
+}  // namespace girih_gpu

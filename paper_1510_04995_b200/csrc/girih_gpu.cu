@@ -1,0 +1,1295 @@
+// girih_gpu.cu -- host runtime and C ABI of the B200 temporally-blocked stencil sweep.
+//
+// Replaces the reference's CPU execution engine girih::run (proj/src/engine.cpp:332-418):
+// instead of std::thread groups pulling diamond tiles from a dependency FIFO
+// (proj/src/scheduler.cpp:27-83), a host-side planner splits the run into passes of up to TB
+// fused time steps, and every pass is one persistent zwave kernel launch per z-slab whose CTAs
+// stream (x,y) tile columns along z (zwave.cuh). Multi-slab handles decompose z across
+// devices (or emulate it on one device) and exchange R*TB-deep halos between passes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <map>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/girih_gpu.h"
+#include "device_api.h"
+#include "variants.h"
+
+using namespace girih_gpu;
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// errors (thread-local message, reference exception classes mapped to status codes)
+// ------------------------------------------------------------------------------------------
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void throw_err(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define GCHECK(expr)                                                                   \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            throw_err(e_ == cudaErrorMemoryAllocation ? GIRIH_ENOMEM : GIRIH_ECUDA,    \
+                      std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return GIRIH_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return GIRIH_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GIRIH_ECUDA;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// traits (proj/src/stencil.cpp:11-17)
+// ------------------------------------------------------------------------------------------
+struct KindInfo {
+    const char* name;
+    int radius, nd, flops, torder, ncoeff;
+    int b1;         // compulsory bytes per LUP of one sweep
+    int dp_ops;     // DMUL + DADD count per LUP in the reference association
+    int default_tb;
+};
+const KindInfo kKinds[4] = {
+    {"const7pt", 1, 2, 7, 1, 0, 16, 10, 4},
+    {"var7pt", 1, 9, 13, 1, 7, 72, 13, 4},
+    {"const25pt", 4, 3, 33, 2, 1, 32, 33, 1},
+    {"var25pt", 4, 15, 37, 1, 13, 120, 37, 1},
+};
+
+const KindInfo& kind_info(int kind) {
+    if (kind < 0 || kind > 3) throw_err(GIRIH_EINVAL, "unknown stencil kind");
+    return kKinds[kind];
+}
+
+const Variant* variant_table(int kind, int* n) {
+    switch (kind) {
+    case K_CONST7: *n = kNumVariantsConst7; return kVariantsConst7;
+    case K_VAR7: *n = kNumVariantsVar7; return kVariantsVar7;
+    case K_CONST25: *n = kNumVariantsConst25; return kVariantsConst25;
+    default: *n = kNumVariantsVar25; return kVariantsVar25;
+    }
+}
+
+int max_tb(int kind) {
+    int n;
+    const Variant* t = variant_table(kind, &n);
+    int m = 1;
+    for (int i = 0; i < n; ++i) m = std::max(m, t[i].tb);
+    return m;
+}
+
+// global variant index: kinds in order, then table order
+const Variant* variant_by_global(int index) {
+    for (int k = 0; k < 4; ++k) {
+        int n;
+        const Variant* t = variant_table(k, &n);
+        if (index < n) return &t[index];
+        index -= n;
+    }
+    return nullptr;
+}
+
+int global_index_of(const Variant* v) {
+    int base = 0;
+    for (int k = 0; k < 4; ++k) {
+        int n;
+        const Variant* t = variant_table(k, &n);
+        if (v >= t && v < t + n) return base + int(v - t);
+        base += n;
+    }
+    return -1;
+}
+
+// pick the variant for (kind, tb, requested global index)
+const Variant* select_variant(int kind, int tb, int requested) {
+    if (requested >= 0) {
+        const Variant* v = variant_by_global(requested);
+        if (!v || v->kind != kind) throw_err(GIRIH_EINVAL, "variant index does not match kind");
+        return v;
+    }
+    int n;
+    const Variant* t = variant_table(kind, &n);
+    for (int i = 0; i < n; ++i)
+        if (t[i].tb == tb) return &t[i];
+    throw_err(GIRIH_EINVAL, "no compiled kernel variant for the requested fused step count");
+}
+
+inline int parity_of(long long t) { return int(((t % 2) + 2) % 2); }
+
+// ------------------------------------------------------------------------------------------
+// host init_value (proj/src/stencil.cpp:19-24, 49-56) -- product copy for the scalars
+// ------------------------------------------------------------------------------------------
+uint64_t splitmix64_h(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+double init_value_h(uint64_t seed, int field, int k, int j, int i) {
+    uint64_t h = splitmix64_h(seed ^ 0x6A09E667F3BCC909ull);
+    h = splitmix64_h(h ^ static_cast<uint64_t>(field));
+    h = splitmix64_h(h ^ static_cast<uint64_t>(static_cast<uint32_t>(k)));
+    h = splitmix64_h(h ^ static_cast<uint64_t>(static_cast<uint32_t>(j)));
+    h = splitmix64_h(h ^ static_cast<uint64_t>(static_cast<uint32_t>(i)));
+    return static_cast<double>(h >> 11) * 0x1.0p-53 - 0.5;
+}
+
+// ------------------------------------------------------------------------------------------
+// pass planner
+// ------------------------------------------------------------------------------------------
+// Buffers: id = slot * 2 + parity; slot 0 = the state's field of that parity (u / v), slot 1
+// = a scratch buffer of that parity. Every buffer's ghost cells hold the pristine ghosts of
+// its parity, so a level of parity p is always stored in a parity-p buffer and ghost reads
+// are uniform (stencil.hpp:78-82: u and v ghosts differ).
+struct Pass {
+    int tb, src, src_prev, dst, dst_penult;
+};
+
+inline int buf_id(int parity, int slot) { return slot * 2 + parity; }
+
+// Minimum-pass planner (dynamic programming over (steps done, source slot)).
+//
+// Jacobi kinds: a pass reads one level and writes one. A pass never writes the buffer it
+// reads; when the output level has the source's parity it must go to the other slot of that
+// parity. The final pass leaves level T in the field of parity(T) and level T-1 in the other
+// field (verify compares u and v, main.cpp:105-127): with TB >= 2 it writes both fields, so
+// its source must be a scratch buffer; a single final step may read a field in place.
+//
+// const25pt leapfrog: a pass reads levels t and t-1 and writes t+TB and t+TB-1. TB = 1 runs in
+// place (U is read and overwritten at the same cell by the same thread, kernels.hpp:50-52);
+// TB >= 2 writes both levels into the other slot of each parity (both slots flip together, so
+// the state is one bit). The run must end with both levels in the fields.
+//
+// Ties prefer the largest fused depth first and field slots over scratch slots.
+std::vector<Pass> plan_dp(int kind, long long t0, long long steps, int tb) {
+    std::vector<Pass> out;
+    if (steps <= 0) return out;
+    const bool leap = (kind == K_CONST25);
+    const long long T = steps;
+    const int INF = 1 << 29;
+    // best[k][a] = min passes to finish from k steps done with source slot a
+    std::vector<std::array<int, 2>> best(size_t(T) + 1, {INF, INF});
+    auto final_ok = [&](long long k, int a, int d) -> bool {
+        if (leap) return (d >= 2 ? (a ^ 1) : a) == 0;
+        (void)k;
+        return d == 1 || a == 1;
+    };
+    // allowed next slots for a non-final pass
+    auto next_slots = [&](long long k, int a, int d, int* b) -> int {
+        if (leap) {
+            b[0] = d >= 2 ? (a ^ 1) : a;
+            return 1;
+        }
+        const int p = parity_of(t0 + k), q = parity_of(t0 + k + d);
+        if (p == q) {
+            b[0] = a ^ 1;
+            return 1;
+        }
+        b[0] = 0;
+        b[1] = 1;
+        return 2;
+    };
+    for (long long k = T - 1; k >= 0; --k)
+        for (int a = 0; a < 2; ++a) {
+            int bestv = INF;
+            for (int d = 1; d <= tb && k + d <= T; ++d) {
+                if (k + d == T) {
+                    if (final_ok(k, a, d)) bestv = std::min(bestv, 1);
+                    continue;
+                }
+                int b[2];
+                const int nb = next_slots(k, a, d, b);
+                for (int i = 0; i < nb; ++i)
+                    if (best[k + d][b[i]] < INF) bestv = std::min(bestv, 1 + best[k + d][b[i]]);
+            }
+            best[k][a] = bestv;
+        }
+    if (best[0][0] >= INF) throw_err(GIRIH_ESTATE, "pass planner found no feasible plan");
+    long long k = 0;
+    int a = 0;
+    int sl_leap = 0;
+    while (k < T) {
+        const int need = best[k][a];
+        int dsel = -1, bsel = -1;
+        for (int d = std::min<long long>(tb, T - k); d >= 1 && dsel < 0; --d) {
+            if (k + d == T) {
+                if (need == 1 && final_ok(k, a, d)) dsel = d;
+                continue;
+            }
+            int b[2];
+            const int nb = next_slots(k, a, d, b);
+            for (int i = 0; i < nb; ++i)
+                if (best[k + d][b[i]] == need - 1) {
+                    dsel = d;
+                    bsel = b[i];
+                    break;
+                }
+        }
+        if (dsel < 0) throw_err(GIRIH_ESTATE, "pass planner reconstruction failed");
+        const long long t = t0 + k;
+        Pass ps{};
+        ps.tb = dsel;
+        if (leap) {
+            ps.src = buf_id(parity_of(t), sl_leap);
+            ps.src_prev = buf_id(parity_of(t - 1), sl_leap);
+            if (dsel == 1) {
+                ps.dst = ps.src_prev;
+                ps.dst_penult = -1;
+            } else {
+                sl_leap ^= 1;
+                ps.dst = buf_id(parity_of(t + dsel), sl_leap);
+                ps.dst_penult = buf_id(parity_of(t + dsel - 1), sl_leap);
+            }
+            a = sl_leap;
+        } else {
+            ps.src = buf_id(parity_of(t), a);
+            ps.src_prev = -1;
+            if (k + dsel == T) {
+                ps.dst = buf_id(parity_of(t + dsel), 0);
+                const bool in_place = (dsel == 1 && a == 0);
+                ps.dst_penult = in_place ? -1 : buf_id(parity_of(t + dsel - 1), 0);
+            } else {
+                ps.dst = buf_id(parity_of(t + dsel), bsel);
+                ps.dst_penult = -1;
+                a = bsel;
+            }
+        }
+        out.push_back(ps);
+        k += dsel;
+    }
+    return out;
+}
+
+std::vector<Pass> make_plan(int kind, long long t0, long long steps, int tb) {
+    if (tb < 1) throw_err(GIRIH_EINVAL, "fused step count must be >= 1");
+    return plan_dp(kind, t0, steps, tb);
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda needed)
+// ------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        GCHECK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000,
+                                                cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+CUtensorMap make_plane_map(const double* base, int pitch, int Y, int Zloc, int lx, int ly) {
+    CUtensorMap map;
+    cuuint64_t dims[3] = {cuuint64_t(pitch), cuuint64_t(Y), cuuint64_t(Zloc)};
+    cuuint64_t strides[2] = {cuuint64_t(pitch) * 8, cuuint64_t(pitch) * Y * 8};
+    cuuint32_t box[3] = {cuuint32_t(lx), cuuint32_t(ly), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = get_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                 const_cast<double*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return map;
+}
+
+// ------------------------------------------------------------------------------------------
+// device state
+// ------------------------------------------------------------------------------------------
+struct DevBuf {
+    double* p = nullptr;
+    int device = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) {
+            cudaSetDevice(device);
+            cudaFree(p);
+        }
+    }
+};
+
+// One z-slab: local planes [0, Zloc) hold global allocated planes [zoff, zoff + Zloc).
+struct Slab {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int Zloc = 0, zoff = 0;
+    int zout_lo = 0, zout_hi = 0;  // own interior planes (local)
+    std::unique_ptr<DevBuf> buf[4];     // u, v, scratch even, scratch odd
+    std::vector<std::unique_ptr<DevBuf>> coeff;
+    cudaEvent_t done = nullptr;    // end of this slab's work in the current pass
+};
+
+struct Handle {
+    int kind = 0, R = 0, nc = 0;
+    int nx = 0, ny = 0, nz = 0, pad_x = 0;
+    int X = 0, Y = 0, Z = 0;
+    int pitch = 0, off = 0;
+    long long t_current = 0;
+    double cc[5] = {0, 0, 0, 0, 0};
+    girih_gpu_config cfg{};
+    int hz = 0;  // halo planes per slab side
+    std::vector<Slab> slabs;
+    bool emulated = false;  // several slabs on one device
+    int sm_count = 0;
+    // timing events (slab 0 stream)
+    std::vector<cudaEvent_t> ev;
+    // cached tensor maps: key (slab, buffer, lx, ly)
+    struct MapEntry {
+        int slab, buf, lx, ly;
+        const double* base;
+        CUtensorMap map;
+    };
+    std::vector<MapEntry> maps;
+
+    size_t plane_elems() const { return size_t(pitch) * Y; }
+    size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
+};
+
+void alloc_buf(std::unique_ptr<DevBuf>& b, int device, size_t elems, cudaStream_t st) {
+    if (b) return;
+    b = std::make_unique<DevBuf>();
+    b->device = device;
+    GCHECK(cudaSetDevice(device));
+    GCHECK(cudaMalloc(&b->p, elems * sizeof(double)));
+    GCHECK(cudaMemsetAsync(b->p, 0, elems * sizeof(double), st));
+}
+
+void setup_geometry(Handle& h, int kind, int nx, int ny, int nz, int pad_x) {
+    const KindInfo& ki = kind_info(kind);
+    const int R = ki.radius;
+    if (nx < 2 * R + 1 || ny < 2 * R + 1 || nz < 2 * R + 1)
+        throw_err(GIRIH_EINVAL, "grid extent below 2R+1 for stencil radius");
+    if (pad_x < 0) throw_err(GIRIH_EINVAL, "negative leading-dimension padding");
+    h.kind = kind;
+    h.R = R;
+    h.nc = ki.ncoeff;
+    h.nx = nx;
+    h.ny = ny;
+    h.nz = nz;
+    h.pad_x = pad_x;
+    h.X = nx + 2 * R + pad_x;
+    h.Y = ny + 2 * R;
+    h.Z = nz + 2 * R;
+    // interior x = R starts on a 128-byte boundary of every device row
+    h.off = (16 - R % 16) % 16;
+    h.pitch = (h.X + h.off + 15) / 16 * 16;
+}
+
+void validate_config(const girih_gpu_config& c, int kind) {
+    if (c.exact != 1) throw_err(GIRIH_EINVAL, "only the bitwise (exact = 1) mode is implemented");
+    if (c.tb < 0 || c.tb > max_tb(kind)) throw_err(GIRIH_EINVAL, "fused step count out of range");
+    if (c.ngpus < 1) throw_err(GIRIH_EINVAL, "ngpus must be >= 1");
+    if (c.zchunks < 0) throw_err(GIRIH_EINVAL, "zchunks must be >= 0");
+    if (c.variant >= 0) {
+        const Variant* v = variant_by_global(c.variant);
+        if (!v || v->kind != kind) throw_err(GIRIH_EINVAL, "variant index does not match kind");
+    }
+}
+
+// Slab layout. ngpus > 1 spreads slabs over devices [device, device + ngpus); the
+// GIRIH_EMULATE_SLABS reserved flag (cfg.reserved > 0) places cfg.reserved slabs on ONE device
+// (used by the single-GPU tests of the decomposition).
+void setup_slabs(Handle& h) {
+    int nslab = h.cfg.ngpus;
+    h.emulated = false;
+    if (h.cfg.reserved > 1 && h.cfg.ngpus == 1) {
+        nslab = h.cfg.reserved;
+        h.emulated = true;
+    }
+    if (nslab > h.nz) throw_err(GIRIH_EINVAL, "more z-slabs than interior planes");
+    int ndev = 0;
+    GCHECK(cudaGetDeviceCount(&ndev));
+    if (!h.emulated && h.cfg.device + nslab > ndev)
+        throw_err(GIRIH_EINVAL, "not enough CUDA devices for ngpus");
+    if (h.cfg.device < 0 || h.cfg.device >= ndev) throw_err(GIRIH_EINVAL, "bad CUDA device");
+    h.hz = (nslab == 1) ? h.R : h.R * max_tb(h.kind);
+    h.slabs.resize(nslab);
+    for (int g = 0; g < nslab; ++g) {
+        Slab& s = h.slabs[g];
+        s.device = h.emulated ? h.cfg.device : h.cfg.device + g;
+        const int z0 = int((long long)h.nz * g / nslab), z1 = int((long long)h.nz * (g + 1) / nslab);
+        if (nslab == 1) {
+            s.Zloc = h.Z;
+            s.zoff = 0;
+            s.zout_lo = h.R;
+            s.zout_hi = h.R + h.nz;
+        } else {
+            s.Zloc = (z1 - z0) + 2 * h.hz;
+            s.zoff = h.R + z0 - h.hz;
+            s.zout_lo = h.hz;
+            s.zout_hi = h.hz + (z1 - z0);
+        }
+        GCHECK(cudaSetDevice(s.device));
+        if (h.emulated && g > 0) {
+            s.stream = h.slabs[0].stream;
+        } else {
+            GCHECK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+            s.own_stream = true;
+        }
+        GCHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+        const size_t n = h.slab_elems(s);
+        alloc_buf(s.buf[0], s.device, n, s.stream);
+        alloc_buf(s.buf[1], s.device, n, s.stream);
+        s.coeff.resize(h.nc);
+        for (int c = 0; c < h.nc; ++c) alloc_buf(s.coeff[c], s.device, n, s.stream);
+    }
+    if (!h.emulated && nslab > 1) {
+        for (int g = 0; g + 1 < nslab; ++g) {
+            int ok = 0;
+            cudaDeviceCanAccessPeer(&ok, h.slabs[g].device, h.slabs[g + 1].device);
+            if (ok) {
+                cudaSetDevice(h.slabs[g].device);
+                cudaError_t e = cudaDeviceEnablePeerAccess(h.slabs[g + 1].device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GCHECK(e);
+                cudaGetLastError();
+                cudaSetDevice(h.slabs[g + 1].device);
+                e = cudaDeviceEnablePeerAccess(h.slabs[g].device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GCHECK(e);
+                cudaGetLastError();
+            }
+        }
+    }
+    GCHECK(cudaSetDevice(h.slabs[0].device));
+    GCHECK(cudaDeviceGetAttribute(&h.sm_count, cudaDevAttrMultiProcessorCount, h.slabs[0].device));
+}
+
+// Ensure scratch buffers of a parity exist (ghost cells copied from the field of that parity).
+void ensure_scratch(Handle& h, int parity) {
+    for (Slab& s : h.slabs) {
+        if (s.buf[2 + parity]) continue;
+        alloc_buf(s.buf[2 + parity], s.device, h.slab_elems(s), s.stream);
+        GCHECK(cudaSetDevice(s.device));
+        GCHECK(cudaMemcpyAsync(s.buf[2 + parity]->p, s.buf[parity]->p,
+                               h.slab_elems(s) * sizeof(double), cudaMemcpyDeviceToDevice,
+                               s.stream));
+    }
+}
+
+// host [k][j][i] (X-pitched) rows <-> device rows for global allocated planes
+void copy_h2d(Handle& h, double* const dev_of_slab[], const double* host) {
+    for (size_t g = 0; g < h.slabs.size(); ++g) {
+        Slab& s = h.slabs[g];
+        // local planes that exist globally
+        const int k0 = std::max(0, -s.zoff), k1 = std::min(s.Zloc, h.Z - s.zoff);
+        if (k1 <= k0) continue;
+        GCHECK(cudaSetDevice(s.device));
+        const double* src = host + (size_t)(k0 + s.zoff) * h.Y * h.X;
+        double* dst = dev_of_slab[g] + (size_t)k0 * h.plane_elems() + h.off;
+        GCHECK(cudaMemcpy2DAsync(dst, size_t(h.pitch) * 8, src, size_t(h.X) * 8, size_t(h.X) * 8,
+                                 size_t(k1 - k0) * h.Y, cudaMemcpyHostToDevice, s.stream));
+    }
+}
+
+void copy_d2h(Handle& h, double* const dev_of_slab[], double* host) {
+    for (size_t g = 0; g < h.slabs.size(); ++g) {
+        Slab& s = h.slabs[g];
+        int k0, k1;  // global planes this slab is authoritative for
+        if (h.slabs.size() == 1) {
+            k0 = 0;
+            k1 = h.Z;
+        } else {
+            k0 = s.zout_lo + s.zoff;
+            k1 = s.zout_hi + s.zoff;
+            if (g == 0) k0 = 0;                          // lower ghost planes
+            if (g + 1 == h.slabs.size()) k1 = h.Z;       // upper ghost planes
+        }
+        GCHECK(cudaSetDevice(s.device));
+        double* dst = host + (size_t)k0 * h.Y * h.X;
+        const double* src = dev_of_slab[g] + (size_t)(k0 - s.zoff) * h.plane_elems() + h.off;
+        GCHECK(cudaMemcpy2DAsync(dst, size_t(h.X) * 8, src, size_t(h.pitch) * 8, size_t(h.X) * 8,
+                                 size_t(k1 - k0) * h.Y, cudaMemcpyDeviceToHost, s.stream));
+    }
+}
+
+void sync_all(Handle& h) {
+    for (Slab& s : h.slabs) {
+        GCHECK(cudaSetDevice(s.device));
+        GCHECK(cudaStreamSynchronize(s.stream));
+    }
+    GCHECK(cudaSetDevice(h.slabs[0].device));
+}
+
+void upload_state(Handle& h, const girih_state_view& v) {
+    if (!v.u || !v.v) throw_err(GIRIH_EINVAL, "state view lacks u/v");
+    if (v.n_coeffs != h.nc) throw_err(GIRIH_EINVAL, "coefficient field count does not match kind");
+    for (int c = 0; c < h.nc; ++c)
+        if (!v.coeffs || !v.coeffs[c]) throw_err(GIRIH_EINVAL, "missing coefficient field");
+    std::vector<double*> d(h.slabs.size());
+    for (int f = 0; f < 2; ++f) {
+        for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].buf[f]->p;
+        copy_h2d(h, d.data(), f == 0 ? v.u : v.v);
+    }
+    for (int c = 0; c < h.nc; ++c) {
+        for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].coeff[c]->p;
+        copy_h2d(h, d.data(), v.coeffs[c]);
+    }
+    std::memcpy(h.cc, v.cc, sizeof h.cc);
+    h.t_current = v.t_current;
+    // refresh existing scratch buffers' ghosts from the new fields
+    for (Slab& s : h.slabs)
+        for (int p = 0; p < 2; ++p)
+            if (s.buf[2 + p]) {
+                GCHECK(cudaSetDevice(s.device));
+                GCHECK(cudaMemcpyAsync(s.buf[2 + p]->p, s.buf[p]->p, h.slab_elems(s) * 8,
+                                       cudaMemcpyDeviceToDevice, s.stream));
+            }
+    sync_all(h);
+}
+
+void init_state_device(Handle& h, uint64_t seed, int remap) {
+    const KindInfo& ki = kind_info(h.kind);
+    double coeff_scale = 1.0;
+    if (h.kind == K_VAR7) coeff_scale = 0.14;
+    if (h.kind == K_VAR25) coeff_scale = 1.0 / 26;
+    for (Slab& s : h.slabs) {
+        GCHECK(cudaSetDevice(s.device));
+        for (int f = 0; f < 2; ++f)
+            GCHECK(launch_init_field(s.buf[f]->p, h.pitch, h.off, h.X, h.Y, s.Zloc, s.zoff, h.Z,
+                                     seed, f, remap, 1.0, s.stream));
+        for (int c = 0; c < ki.ncoeff; ++c)
+            GCHECK(launch_init_field(s.coeff[c]->p, h.pitch, h.off, h.X, h.Y, s.Zloc, s.zoff, h.Z,
+                                     seed, 2 + c, remap, coeff_scale, s.stream));
+    }
+    for (int c = 0; c < 5; ++c) h.cc[c] = init_value_h(seed, 64, 0, 0, c);
+    if (remap) {
+        // SURVEY.md 8(d) scalar remaps (same expressions as the oracle restatement)
+        if (h.kind == K_CONST7) {
+            h.cc[0] = (h.cc[0] + 0.5) * 0.2;
+            h.cc[1] = (h.cc[1] + 0.5) * 0.2;
+        } else if (h.kind == K_CONST25) {
+            double r[5];
+            for (int c = 0; c < 5; ++c) r[c] = h.cc[c] + 0.5;
+            const double s = 0.99 / (r[0] + 6 * (r[1] + r[2] + r[3] + r[4]));
+            for (int c = 0; c < 5; ++c) h.cc[c] = r[c] * s;
+        }
+    }
+    h.t_current = 0;
+    sync_all(h);
+}
+
+const CUtensorMap& plane_map(Handle& h, int slab, int buf, int lx, int ly) {
+    const double* base = h.slabs[slab].buf[buf]->p;
+    for (auto& m : h.maps)
+        if (m.slab == slab && m.buf == buf && m.lx == lx && m.ly == ly && m.base == base) return m.map;
+    h.maps.push_back({slab, buf, lx, ly, base,
+                      make_plane_map(base, h.pitch, h.Y, h.slabs[slab].Zloc, lx, ly)});
+    return h.maps.back().map;
+}
+
+// z chunks per tile column: minimise (waves of units) x (planes streamed per unit)
+int choose_zchunks(int tiles_xy, int nzl, int grid, int H) {
+    int best = 1;
+    double best_cost = 1e300;
+    const int max_chunks = std::max(1, nzl / std::max(8, 2 * H));
+    for (int c = 1; c <= max_chunks; ++c) {
+        const int len = (nzl + c - 1) / c;
+        const long long units = (long long)tiles_xy * c;
+        const long long waves = (units + grid - 1) / grid;
+        const double cost = double(waves) * double(len + 2 * H);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = c;
+        }
+    }
+    return best;
+}
+
+struct LaunchInfo {
+    int grid = 0, zchunks = 0;
+    long long computed_lups = 0;
+};
+
+// Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
+PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_index,
+                        long long t0, LaunchInfo* li) {
+    Slab& s = h.slabs[slab_index];
+    const int R = h.R, H = ps.tb * R;
+    const int OX = var->lx - 2 * H, OY = var->ly - 2 * H;
+    PassParams p{};
+    p.src_prev = ps.src_prev >= 0 ? s.buf[ps.src_prev]->p : nullptr;
+    p.dst_final = s.buf[ps.dst]->p;
+    p.dst_penult = ps.dst_penult >= 0 ? s.buf[ps.dst_penult]->p : nullptr;
+    p.ghost[0] = s.buf[0]->p;
+    p.ghost[1] = s.buf[1]->p;
+    for (int c = 0; c < h.nc; ++c) p.coeff[c] = s.coeff[c]->p;
+    for (int c = 0; c < 5; ++c) p.cc[c] = h.cc[c];
+    p.parity0 = parity_of(t0);
+    p.nx = h.nx;
+    p.ny = h.ny;
+    p.X = h.X;
+    p.Y = h.Y;
+    p.pitch = h.pitch;
+    p.off = h.off;
+    p.plane = (long long)h.pitch * h.Y;
+    p.Zloc = s.Zloc;
+    p.zoff = s.zoff;
+    p.nzg = h.nz;
+    p.tiles_x = (h.nx + OX - 1) / OX;
+    p.tiles_y = (h.ny + OY - 1) / OY;
+    p.zout_lo = s.zout_lo;
+    p.zout_hi = s.zout_hi;
+    const int nzl = s.zout_hi - s.zout_lo;
+    int occ = 1;
+    GCHECK(var->occupancy(&occ));
+    if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
+    const int max_grid = h.sm_count * occ;
+    const int txy = p.tiles_x * p.tiles_y;
+    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
+                              : choose_zchunks(txy, nzl, max_grid, H);
+    p.zc_len = (nzl + p.nzc - 1) / p.nzc;
+    p.nzc = (nzl + p.zc_len - 1) / p.zc_len;
+    p.units = txy * p.nzc;
+    li->grid = std::min(p.units, max_grid);
+    li->zchunks = p.nzc;
+    // computed LUPs: level s covers (OX + 2(TB-s)R) x (OY + 2(TB-s)R) per tile column and
+    // nzl + 2 nzc (TB-s) R planes
+    li->computed_lups = 0;
+    for (int lev = 1; lev <= ps.tb; ++lev) {
+        const long long ex = (long long)(OX + 2 * (ps.tb - lev) * R);
+        const long long ey = (long long)(OY + 2 * (ps.tb - lev) * R);
+        const long long ez = (long long)nzl + 2LL * p.nzc * (ps.tb - lev) * R;
+        li->computed_lups += ex * ey * (long long)txy * ez;
+    }
+    return p;
+}
+
+}  // namespace
+
+// Out-of-namespace helpers that need PassParams parity (kept separate for clarity)
+namespace {
+
+struct StepStats {
+    int n_launches = 0;
+    double pass_s = 0;
+    long long computed = 0;
+    int grid = 0, zchunks = 0, variant = -1, tb_used = 0;
+};
+
+void exchange_halos(Handle& h, int buf) {
+    const int ns = int(h.slabs.size());
+    if (ns < 2) return;
+    const size_t pe = h.plane_elems();
+    const int hz = h.hz;
+    for (int g = 0; g < ns; ++g) GCHECK(cudaEventRecord(h.slabs[g].done, h.slabs[g].stream));
+    for (int g = 0; g < ns; ++g) {
+        Slab& s = h.slabs[g];
+        GCHECK(cudaSetDevice(s.device));
+        if (g > 0) {  // my lower halo <- top hz own planes of slab g-1
+            Slab& n = h.slabs[g - 1];
+            if (!h.emulated) GCHECK(cudaStreamWaitEvent(s.stream, n.done, 0));
+            GCHECK(cudaMemcpyPeerAsync(s.buf[buf]->p, s.device,
+                                       n.buf[buf]->p + (size_t)(n.zout_hi - hz) * pe, n.device,
+                                       (size_t)hz * pe * 8, s.stream));
+        }
+        if (g + 1 < ns) {  // my upper halo <- bottom hz own planes of slab g+1
+            Slab& n = h.slabs[g + 1];
+            if (!h.emulated) GCHECK(cudaStreamWaitEvent(s.stream, n.done, 0));
+            GCHECK(cudaMemcpyPeerAsync(s.buf[buf]->p + (size_t)s.zout_hi * pe, s.device,
+                                       n.buf[buf]->p + (size_t)n.zout_lo * pe, n.device,
+                                       (size_t)hz * pe * 8, s.stream));
+        }
+    }
+}
+
+StepStats do_step(Handle& h, long long steps, bool time_passes) {
+    StepStats st;
+    if (steps == 0) return st;
+    const int tb = h.cfg.tb > 0 ? h.cfg.tb : kKinds[h.kind].default_tb;
+    std::vector<Pass> plan = make_plan(h.kind, h.t_current, steps, tb);
+    for (const Pass& ps : plan) {
+        for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
+            if (b >= 2) ensure_scratch(h, b & 1);
+    }
+    if (time_passes) {
+        const size_t need = 2 * plan.size();
+        GCHECK(cudaSetDevice(h.slabs[0].device));
+        while (h.ev.size() < need) {
+            cudaEvent_t e;
+            GCHECK(cudaEventCreate(&e));
+            h.ev.push_back(e);
+        }
+    }
+    long long t = h.t_current;
+    int pi = 0;
+    for (const Pass& ps : plan) {
+        const Variant* var =
+            select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
+        if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+        st.variant = global_index_of(var);
+        st.tb_used = std::max(st.tb_used, ps.tb);
+        for (size_t g = 0; g < h.slabs.size(); ++g) {
+            Slab& s = h.slabs[g];
+            GCHECK(cudaSetDevice(s.device));
+            LaunchInfo li;
+            const PassParams p = build_params(h, ps, var, int(g), t, &li);
+            const CUtensorMap& map = plane_map(h, int(g), ps.src, var->lx, var->ly);
+            if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi], s.stream));
+            GCHECK(var->launch(map, p, li.grid, s.stream));
+            if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi + 1], s.stream));
+            st.computed += li.computed_lups;
+            st.grid = li.grid;
+            st.zchunks = li.zchunks;
+            st.n_launches++;
+        }
+        // halo exchange of the levels the next pass reads
+        if (h.slabs.size() > 1) {
+            exchange_halos(h, ps.dst);
+            if (h.kind == K_CONST25 && ps.dst_penult >= 0) exchange_halos(h, ps.dst_penult);
+        }
+        t += ps.tb;
+        ++pi;
+    }
+    h.t_current = t;
+    if (time_passes) {
+        sync_all(h);
+        for (int i = 0; i < pi; ++i) {
+            float ms = 0;
+            GCHECK(cudaEventElapsedTime(&ms, h.ev[2 * i], h.ev[2 * i + 1]));
+            st.pass_s += ms * 1e-3;
+        }
+    }
+    return st;
+}
+
+Handle* as_handle(void* p) {
+    if (!p) throw_err(GIRIH_ESTATE, "null handle");
+    return static_cast<Handle*>(p);
+}
+
+girih_gpu_config default_config() {
+    girih_gpu_config c{};
+    c.tb = 0;
+    c.variant = -1;
+    c.zchunks = 0;
+    c.ngpus = 1;
+    c.exact = 1;
+    c.device = 0;
+    c.graphs = 0;
+    c.reserved = 0;
+    return c;
+}
+
+void destroy(Handle* h) {
+    for (Slab& s : h->slabs) {
+        cudaSetDevice(s.device);
+        if (s.stream) cudaStreamSynchronize(s.stream);
+        if (s.done) cudaEventDestroy(s.done);
+    }
+    for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+    for (Slab& s : h->slabs) {
+        for (auto& b : s.buf) b.reset();
+        s.coeff.clear();
+        if (s.own_stream && s.stream) {
+            cudaSetDevice(s.device);
+            cudaStreamDestroy(s.stream);
+        }
+    }
+    delete h;
+}
+
+double step_timed(Handle& h, long long steps, girih_gpu_report* rep) {
+    const auto w0 = std::chrono::steady_clock::now();
+    // device-clock timing: events around all work, per slab; take the max over slabs
+    std::vector<cudaEvent_t> e0(h.slabs.size()), e1(h.slabs.size());
+    for (size_t g = 0; g < h.slabs.size(); ++g) {
+        GCHECK(cudaSetDevice(h.slabs[g].device));
+        GCHECK(cudaEventCreate(&e0[g]));
+        GCHECK(cudaEventCreate(&e1[g]));
+        GCHECK(cudaEventRecord(e0[g], h.slabs[g].stream));
+    }
+    StepStats st = do_step(h, steps, rep != nullptr);
+    for (size_t g = 0; g < h.slabs.size(); ++g) {
+        GCHECK(cudaSetDevice(h.slabs[g].device));
+        GCHECK(cudaEventRecord(e1[g], h.slabs[g].stream));
+    }
+    sync_all(h);
+    double ksec = 0;
+    for (size_t g = 0; g < h.slabs.size(); ++g) {
+        float ms = 0;
+        GCHECK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+        ksec = std::max(ksec, ms * 1e-3);
+        cudaEventDestroy(e0[g]);
+        cudaEventDestroy(e1[g]);
+    }
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    if (rep) {
+        std::memset(rep, 0, sizeof *rep);
+        const KindInfo& ki = kKinds[h.kind];
+        rep->wall_s = wall;
+        rep->kernel_s = ksec;
+        rep->lups = (long long)h.nx * h.ny * h.nz * steps;
+        rep->mlups = ksec > 0 ? rep->lups / ksec / 1e6 : 0.0;
+        rep->tb_used = st.tb_used;
+        rep->model_bytes_per_lup = st.tb_used > 0 ? double(ki.b1) / st.tb_used : 0.0;
+        rep->n_launches = st.n_launches;
+        rep->pass_s = st.pass_s;
+        rep->computed_lups = st.computed;
+        rep->variant_used = st.variant;
+        rep->zchunks_used = st.zchunks;
+        rep->grid_ctas = st.grid;
+    }
+    return ksec;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+const char* girih_gpu_last_error(void) { return g_err.c_str(); }
+
+int girih_gpu_abi_version(void) { return GIRIH_GPU_ABI_VERSION; }
+
+int girih_gpu_traits(int kind, int* radius, int* domain_streams, int* flops_per_lup,
+                     int* time_order, int* coeff_arrays) {
+    return guarded([&] {
+        const KindInfo& k = kind_info(kind);
+        if (radius) *radius = k.radius;
+        if (domain_streams) *domain_streams = k.nd;
+        if (flops_per_lup) *flops_per_lup = k.flops;
+        if (time_order) *time_order = k.torder;
+        if (coeff_arrays) *coeff_arrays = k.ncoeff;
+    });
+}
+
+int girih_gpu_kind_from_name(const char* name, int* kind) {
+    return guarded([&] {
+        if (!name || !kind) throw_err(GIRIH_EINVAL, "null argument");
+        for (int i = 0; i < 4; ++i)
+            if (std::strcmp(name, kKinds[i].name) == 0) {
+                *kind = i;
+                return;
+            }
+        throw_err(GIRIH_EINVAL, std::string("unknown stencil kind: ") + name);
+    });
+}
+
+int girih_gpu_variant_count(void) {
+    int total = 0;
+    for (int k = 0; k < 4; ++k) {
+        int n;
+        variant_table(k, &n);
+        total += n;
+    }
+    return total;
+}
+
+int girih_gpu_variant_info(int index, girih_gpu_variant* out) {
+    return guarded([&] {
+        const Variant* v = variant_by_global(index);
+        if (!v || !out) throw_err(GIRIH_EINVAL, "variant index out of range");
+        out->kind = v->kind;
+        out->tb = v->tb;
+        out->lx = v->lx;
+        out->ly = v->ly;
+        out->threads = v->threads;
+        out->prefetch = v->prefetch;
+        out->smem_bytes = v->smem_bytes;
+    });
+}
+
+int girih_gpu_open(const girih_state_view* state, const girih_gpu_config* cfg, void** handle) {
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!state || !handle) throw_err(GIRIH_EINVAL, "null argument");
+        h = new Handle();
+        h->cfg = cfg ? *cfg : default_config();
+        setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        upload_state(*h, *state);
+        *handle = h;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_open_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned long long seed,
+                          int remap, const girih_gpu_config* cfg, void** handle) {
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!handle) throw_err(GIRIH_EINVAL, "null argument");
+        h = new Handle();
+        h->cfg = cfg ? *cfg : default_config();
+        setup_geometry(*h, kind, nx, ny, nz, pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        init_state_device(*h, seed, remap);
+        *handle = h;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_upload(void* handle, const girih_state_view* state) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!state || state->kind != h.kind || state->nx != h.nx || state->ny != h.ny ||
+            state->nz != h.nz || state->pad_x != h.pad_x)
+            throw_err(GIRIH_EINVAL, "state view does not match the handle");
+        upload_state(h, *state);
+    });
+}
+
+int girih_gpu_step(void* handle, long long steps, girih_gpu_report* report) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
+        step_timed(h, steps, report);
+    });
+}
+
+int girih_gpu_download(void* handle, girih_state_view* state) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!state) throw_err(GIRIH_EINVAL, "null argument");
+        std::vector<double*> d(h.slabs.size());
+        for (int f = 0; f < 2; ++f) {
+            double* dst = f == 0 ? state->u : state->v;
+            if (!dst) continue;
+            for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].buf[f]->p;
+            copy_d2h(h, d.data(), dst);
+        }
+        sync_all(h);
+        state->t_current = h.t_current;
+        std::memcpy(state->cc, h.cc, sizeof h.cc);
+    });
+}
+
+int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double* cc) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (n > h.nc) throw_err(GIRIH_EINVAL, "more coefficient fields requested than exist");
+        std::vector<double*> d(h.slabs.size());
+        for (int c = 0; c < n; ++c) {
+            if (!coeffs || !coeffs[c]) continue;
+            for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].coeff[c]->p;
+            copy_d2h(h, d.data(), coeffs[c]);
+        }
+        sync_all(h);
+        if (cc) std::memcpy(cc, h.cc, sizeof h.cc);
+    });
+}
+
+int girih_gpu_get_t(void* handle, long long* t) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!t) throw_err(GIRIH_EINVAL, "null argument");
+        *t = h.t_current;
+    });
+}
+
+int girih_gpu_set_config(void* handle, const girih_gpu_config* cfg) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!cfg) throw_err(GIRIH_EINVAL, "null argument");
+        if (cfg->ngpus != h.cfg.ngpus || cfg->device != h.cfg.device ||
+            cfg->reserved != h.cfg.reserved)
+            throw_err(GIRIH_EINVAL, "device layout cannot change on an open handle");
+        validate_config(*cfg, h.kind);
+        h.cfg = *cfg;
+    });
+}
+
+int girih_gpu_close(void* handle) {
+    return guarded([&] {
+        if (!handle) return;
+        destroy(static_cast<Handle*>(handle));
+    });
+}
+
+int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
+                  girih_gpu_report* report) {
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!state) throw_err(GIRIH_EINVAL, "null argument");
+        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
+        // validate the kind/extents first so errors match girih::run's invalid_argument
+        {
+            Handle probe;
+            setup_geometry(probe, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        }
+        if (steps == 0) {  // engine.cpp:340-341: no work, no state change
+            if (report) {
+                std::memset(report, 0, sizeof *report);
+            }
+            return;
+        }
+        const auto w0 = std::chrono::steady_clock::now();
+        h = new Handle();
+        h->cfg = cfg ? *cfg : default_config();
+        setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        const auto a0 = std::chrono::steady_clock::now();
+        upload_state(*h, *state);
+        const auto a1 = std::chrono::steady_clock::now();
+        girih_gpu_report r{};
+        step_timed(*h, steps, &r);
+        const auto b0 = std::chrono::steady_clock::now();
+        std::vector<double*> d(h->slabs.size());
+        for (int f = 0; f < 2; ++f) {
+            for (size_t g = 0; g < h->slabs.size(); ++g) d[g] = h->slabs[g].buf[f]->p;
+            copy_d2h(*h, d.data(), f == 0 ? state->u : state->v);
+        }
+        sync_all(*h);
+        const auto b1 = std::chrono::steady_clock::now();
+        state->t_current = h->t_current;
+        if (report) {
+            *report = r;
+            const size_t cells = size_t(h->X) * h->Y * h->Z;
+            report->h2d_s = std::chrono::duration<double>(a1 - a0).count();
+            report->d2h_s = std::chrono::duration<double>(b1 - b0).count();
+            report->h2d_bytes = (long long)(cells * 8 * (2 + h->nc));
+            report->d2h_bytes = (long long)(cells * 8 * 2);
+            report->wall_s = std::chrono::duration<double>(b1 - w0).count();
+            report->mlups = report->wall_s > 0 ? report->lups / report->wall_s / 1e6 : 0.0;
+        }
+        destroy(h);
+        h = nullptr;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_passes, int* n_passes,
+                   int* pass_tb, int* pass_src, int* pass_src_prev, int* pass_dst,
+                   int* pass_dst_penult) {
+    return guarded([&] {
+        kind_info(kind);
+        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
+        std::vector<Pass> plan = make_plan(kind, t0, steps, tb);
+        if (n_passes) *n_passes = int(plan.size());
+        if (int(plan.size()) > max_passes) throw_err(GIRIH_EINVAL, "plan longer than max_passes");
+        for (size_t i = 0; i < plan.size(); ++i) {
+            if (pass_tb) pass_tb[i] = plan[i].tb;
+            if (pass_src) pass_src[i] = plan[i].src;
+            if (pass_src_prev) pass_src_prev[i] = plan[i].src_prev;
+            if (pass_dst) pass_dst[i] = plan[i].dst;
+            if (pass_dst_penult) pass_dst_penult[i] = plan[i].dst_penult;
+        }
+    });
+}
+
+int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double* best_mlups,
+                   int* n_measured) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!best) throw_err(GIRIH_EINVAL, "null argument");
+        const int tb_cap = std::max(1, std::min(max_tb_req > 0 ? max_tb_req : 64, max_tb(h.kind)));
+        // snapshot the solution fields so tuning leaves the state untouched (the reference
+        // tunes on scratch state, make_engine_measure, proj/src/tuner.cpp:212-223)
+        const long long t_saved = h.t_current;
+        std::vector<std::unique_ptr<DevBuf>> snap;
+        for (Slab& s : h.slabs)
+            for (int f = 0; f < 2; ++f) {
+                snap.emplace_back();
+                alloc_buf(snap.back(), s.device, h.slab_elems(s), s.stream);
+                GCHECK(cudaMemcpyAsync(snap.back()->p, s.buf[f]->p, h.slab_elems(s) * 8,
+                                       cudaMemcpyDeviceToDevice, s.stream));
+            }
+        const girih_gpu_config cfg_saved = h.cfg;
+        int measured = 0;
+        // candidates: compiled variants of this kind with tb <= cap, times z-chunk choices
+        int nv;
+        const Variant* vt = variant_table(h.kind, &nv);
+        std::vector<int> vars;
+        for (int i = 0; i < nv; ++i)
+            if (vt[i].tb <= tb_cap) vars.push_back(global_index_of(&vt[i]));
+        const int zopts[] = {0, 1, 2, 4, 8, 16};
+        const int nz_opts = int(sizeof(zopts) / sizeof(zopts[0]));
+        std::map<std::pair<int, int>, double> seen;
+        // adaptive_measure (tuner.cpp:47-71): double the test size until two runs agree
+        auto measure = [&](int vi, int zi) -> double {
+            auto key = std::make_pair(vi, zi);
+            if (auto it = seen.find(key); it != seen.end()) return it->second;
+            const Variant* v = variant_by_global(vars[vi]);
+            girih_gpu_config c = cfg_saved;
+            c.tb = v->tb;
+            c.variant = vars[vi];
+            c.zchunks = zopts[zi];
+            h.cfg = c;
+            long long steps = 2LL * v->tb;
+            girih_gpu_report r{};
+            step_timed(h, steps, &r);  // warm-up
+            double last = 0;
+            step_timed(h, steps, &r);
+            last = r.mlups;
+            for (int rep = 1; rep < 6; ++rep) {
+                steps *= 2;
+                step_timed(h, steps, &r);
+                const double next = r.mlups;
+                const bool close = std::abs(next - last) / std::max(last, 1e-300) < 0.05;
+                last = next;
+                if (close) break;
+            }
+            ++measured;
+            seen.emplace(key, last);
+            return last;
+        };
+        // hill_climb (tuner.cpp:73-104): axis-aligned, strict improvement, memoised
+        int bv = 0, bz = 0;
+        for (size_t i = 0; i < vars.size(); ++i)  // start at the largest fused depth
+            if (variant_by_global(vars[i])->tb >= variant_by_global(vars[bv])->tb) bv = int(i);
+        double bs = measure(bv, bz);
+        while (true) {
+            int nv2 = bv, nz2 = bz;
+            double ns = bs;
+            const int cand[4][2] = {{bv - 1, bz}, {bv + 1, bz}, {bv, bz - 1}, {bv, bz + 1}};
+            for (auto& c : cand) {
+                if (c[0] < 0 || c[0] >= int(vars.size()) || c[1] < 0 || c[1] >= nz_opts) continue;
+                const double sc = measure(c[0], c[1]);
+                if (sc > ns) {
+                    ns = sc;
+                    nv2 = c[0];
+                    nz2 = c[1];
+                }
+            }
+            if (nv2 == bv && nz2 == bz) break;
+            bv = nv2;
+            bz = nz2;
+            bs = ns;
+        }
+        // restore
+        size_t q = 0;
+        for (Slab& s : h.slabs)
+            for (int f = 0; f < 2; ++f, ++q)
+                GCHECK(cudaMemcpyAsync(s.buf[f]->p, snap[q]->p, h.slab_elems(s) * 8,
+                                       cudaMemcpyDeviceToDevice, s.stream));
+        sync_all(h);
+        h.t_current = t_saved;
+        h.cfg = cfg_saved;
+        *best = cfg_saved;
+        best->tb = variant_by_global(vars[bv])->tb;
+        best->variant = vars[bv];
+        best->zchunks = zopts[bz];
+        if (best_mlups) *best_mlups = bs;
+        if (n_measured) *n_measured = measured;
+    });
+}
+
+int girih_gpu_host_alloc(size_t bytes, void** ptr) {
+    return guarded([&] {
+        if (!ptr) throw_err(GIRIH_EINVAL, "null argument");
+        GCHECK(cudaMallocHost(ptr, bytes));
+    });
+}
+
+int girih_gpu_host_free(void* ptr) {
+    return guarded([&] { GCHECK(cudaFreeHost(ptr)); });
+}
+
+int girih_gpu_interior_checksum(const girih_state_view* s, unsigned long long* out) {
+    return guarded([&] {
+        if (!s || !out) throw_err(GIRIH_EINVAL, "null argument");
+        const KindInfo& k = kind_info(s->kind);
+        const int R = k.radius;
+        const size_t X = size_t(s->nx) + 2 * R + s->pad_x, Y = size_t(s->ny) + 2 * R;
+        const double* f = (s->t_current % 2 == 0) ? s->u : s->v;
+        uint64_t hsh = 0xCBF29CE484222325ull;
+        for (int kk = R; kk < R + s->nz; ++kk)
+            for (int j = R; j < R + s->ny; ++j)
+                for (int i = R; i < R + s->nx; ++i) {
+                    uint64_t bits;
+                    std::memcpy(&bits, &f[(size_t(kk) * Y + j) * X + i], 8);
+                    for (int b = 0; b < 8; ++b) {
+                        hsh ^= (bits >> (8 * b)) & 0xFF;
+                        hsh *= 0x100000001B3ull;
+                    }
+                }
+        *out = hsh;
+    });
+}
+
+int girih_gpu_fp64_peak(int device, double* addmul, double* fma) {
+    return guarded([&] {
+        GCHECK(cudaSetDevice(device));
+        int sms = 0;
+        GCHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        double* out = nullptr;
+        GCHECK(cudaMalloc(&out, 8));
+        cudaStream_t st;
+        GCHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t a, b;
+        GCHECK(cudaEventCreate(&a));
+        GCHECK(cudaEventCreate(&b));
+        const int blocks = sms * 8, threads = 256, iters = 4096;
+        double res[2] = {0, 0};
+        for (int mode = 0; mode < 2; ++mode) {
+            GCHECK(launch_fp64_probe(mode, out, blocks, threads, 64, st));  // warm-up
+            float best = 1e30f;
+            for (int rep = 0; rep < 3; ++rep) {
+                GCHECK(cudaEventRecord(a, st));
+                GCHECK(launch_fp64_probe(mode, out, blocks, threads, iters, st));
+                GCHECK(cudaEventRecord(b, st));
+                GCHECK(cudaEventSynchronize(b));
+                float ms;
+                GCHECK(cudaEventElapsedTime(&ms, a, b));
+                best = std::min(best, ms);
+            }
+            // 8 chains x 8 unrolled x iters steps per thread; 2 ops (or 2 flops) per step
+            const double ops = 2.0 * 8 * 8 * double(iters) * blocks * threads;
+            res[mode] = ops / (best * 1e-3);
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(st);
+        cudaFree(out);
+        if (addmul) *addmul = res[0];
+        if (fma) *fma = res[1];
+    });
+}
+
+int girih_gpu_device_info(int device, int* sm_count, char* name, int name_len) {
+    return guarded([&] {
+        cudaDeviceProp prop;
+        GCHECK(cudaGetDeviceProperties(&prop, device));
+        if (sm_count) *sm_count = prop.multiProcessorCount;
+        if (name && name_len > 0) {
+            std::strncpy(name, prop.name, size_t(name_len) - 1);
+            name[name_len - 1] = 0;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// init_kernels.cu -- device-side counter-based initialisation and FP64 rate probe.
+//
+// init_value (proj/src/stencil.cpp:19-24, 49-56) is pure 64-bit integer mixing plus an exact
+// conversion, so the device reproduces the host generator bit for bit; each GPU fills its own
+// z-slab (keyed on global (k, j, i)) without any host fill or H2D of the state.
+#include <cstdint>
+
+#include "device_api.h"
+
+namespace girih_gpu {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ double init_value_dev(uint64_t seed, int field, int k, int j, int i) {
+    uint64_t h = splitmix64(seed ^ 0x6A09E667F3BCC909ull);
+    h = splitmix64(h ^ static_cast<uint64_t>(field));
+    h = splitmix64(h ^ static_cast<uint64_t>(static_cast<uint32_t>(k)));
+    h = splitmix64(h ^ static_cast<uint64_t>(static_cast<uint32_t>(j)));
+    h = splitmix64(h ^ static_cast<uint64_t>(static_cast<uint32_t>(i)));
+    return __dsub_rn(__dmul_rn(static_cast<double>(h >> 11), 0x1.0p-53), 0.5);
+}
+
+// Fills local planes [0, Zloc) of a device-layout buffer. Global allocated plane of local
+// plane k is k + zoff; cells outside the global allocation are left untouched.
+__global__ void init_field_kernel(double* buf, int pitch, int off, int X, int Y, int Zloc,
+                                  int zoff, int Zg, uint64_t seed, int field, int remap,
+                                  double scale) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int k = blockIdx.z;
+    if (i >= X || j >= Y || k >= Zloc) return;
+    const int kg = k + zoff;
+    if (kg < 0 || kg >= Zg) return;
+    double v = init_value_dev(seed, field, kg, j, i);
+    // SURVEY.md 8(d) remap: fields x + 0.5 (scale 1), coefficient grids (x + 0.5) * scale
+    if (remap) v = __dmul_rn(__dadd_rn(v, 0.5), scale);
+    buf[(static_cast<long long>(k) * Y + j) * pitch + off + i] = v;
+}
+
+cudaError_t launch_init_field(double* buf, int pitch, int off, int X, int Y, int Zloc, int zoff,
+                              int Zg, uint64_t seed, int field, int remap, double scale,
+                              cudaStream_t stream) {
+    dim3 block(128);
+    dim3 grid((X + 127) / 128, Y, Zloc);
+    init_field_kernel<<<grid, block, 0, stream>>>(buf, pitch, off, X, Y, Zloc, zoff, Zg, seed,
+                                                  field, remap, scale);
+    return cudaGetLastError();
+}
+
+// ---- FP64 rate probe: independent chains of DADD/DMUL (bitwise mode) or DFMA ----
+template <int MODE>
+__global__ void fp64_probe_kernel(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int n = 0; n < iters; ++n) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (MODE == 0) {
+                x0 = __dadd_rn(__dmul_rn(x0, a), b); x1 = __dadd_rn(__dmul_rn(x1, a), b);
+                x2 = __dadd_rn(__dmul_rn(x2, a), b); x3 = __dadd_rn(__dmul_rn(x3, a), b);
+                x4 = __dadd_rn(__dmul_rn(x4, a), b); x5 = __dadd_rn(__dmul_rn(x5, a), b);
+                x6 = __dadd_rn(__dmul_rn(x6, a), b); x7 = __dadd_rn(__dmul_rn(x7, a), b);
+            } else {
+                x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b);
+                x3 = __fma_rn(x3, a, b); x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b);
+                x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+            }
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+cudaError_t launch_fp64_probe(int mode, double* out, int blocks, int threads, int iters,
+                              cudaStream_t stream) {
+    if (mode == 0)
+        fp64_probe_kernel<0><<<blocks, threads, 0, stream>>>(out, iters, 0.999999, 1e-7);
+    else
+        fp64_probe_kernel<1><<<blocks, threads, 0, stream>>>(out, iters, 0.999999, 1e-7);
+    return cudaGetLastError();
+}
+
+}  // namespace girih_gpu

@@ -1,0 +1,12 @@
+// variants_const25.cu -- zwave instantiations for const25 (kept in its own TU so nvcc builds kinds in parallel).
+#include "variants.h"
+
+namespace girih_gpu {
+
+const Variant kVariantsConst25[] = {
+    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 512, 2),
+    GIRIH_VARIANT(K_CONST25, 2, 32, 32, 256, 2),
+};
+const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
+
+}  // namespace girih_gpu

@@ -1,0 +1,246 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle, bitwise, in u AND v
+(ghosts and pad included) -- the reference's verify contract (proj/tools/main.cpp:105-142)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bindings import TRAITS
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def to_problem(g, hs):
+    return g.ProblemState(hs.kind, g.GridSpec(hs.nx, hs.ny, hs.nz, hs.pad_x), hs.u.copy(),
+                          hs.v.copy(), [c.copy() for c in hs.coeffs], hs.cc.copy(), hs.t_current)
+
+
+def assert_state_equal(st, ref, what=""):
+    assert st.t_current == ref.t_current, what
+    for name in ("u", "v"):
+        a = getattr(st, name).view(np.uint64)
+        b = getattr(ref, name).view(np.uint64)
+        if not np.array_equal(a, b):
+            idx = np.argwhere(a != b)
+            k, j, i = idx[0]
+            raise AssertionError(
+                f"{what}: field {name} differs at {len(idx)} cells, first (i,j,k)=({i},{j},{k}) "
+                f"oracle={getattr(ref, name)[k, j, i]!r} gpu={getattr(st, name)[k, j, i]!r}")
+
+
+def tbs_for(g, kind):
+    return sorted({v["tb"] for v in g.variants() if v["kind"] == kind})
+
+
+KIND_IDS = ["const7pt", "var7pt", "const25pt", "var25pt"]
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_run_matches_oracle_every_tb(girih, oracle, kind):
+    g = girih
+    dims = (37, 29, 31, 3) if kind < 2 else (35, 27, 29, 2)
+    base = oracle.init_state(kind, *dims, 11, remap=True)
+    for tb in tbs_for(g, kind):
+        for steps in (1, 2, tb + 1, 3 * tb + 1):
+            ref = base.copy()
+            oracle.naive_sweep(ref, steps)
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb))
+            assert_state_equal(st, ref, f"{KIND_IDS[kind]} tb={tb} T={steps}")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_continuation_odd_start_and_padding(girih, oracle, kind):
+    # test_engine.cpp:149-157: a second run continues from the previous level; pad_x = 2
+    g = girih
+    n = 16 if kind < 2 else 17
+    base = oracle.init_state(kind, n, n, n, 2, 9)
+    ref = base.copy()
+    oracle.naive_sweep(ref, 7)
+    st = to_problem(g, base)
+    tbmax = max(tbs_for(g, kind))
+    g.run(st, 3, g.GpuConfig(tb=min(2, tbmax)))
+    g.run(st, 4, g.GpuConfig(tb=tbmax))
+    assert_state_equal(st, ref, "continuation")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_zchunks_forced(girih, oracle, kind):
+    # z-chunked work units recompute an R*TB-deep z halo (trapezoid in z); results unchanged
+    g = girih
+    dims = (30, 22, 41, 0)
+    base = oracle.init_state(kind, *dims, 5, remap=True)
+    tb = max(tbs_for(g, kind))
+    ref = base.copy()
+    oracle.naive_sweep(ref, 2 * tb + 1)
+    for zc in (1, 2, 3, 7, 41):
+        st = to_problem(g, base)
+        g.run(st, 2 * tb + 1, g.GpuConfig(tb=tb, zchunks=zc))
+        assert_state_equal(st, ref, f"zchunks={zc}")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_every_variant(girih, oracle, kind):
+    g = girih
+    base = oracle.init_state(kind, 40, 36, 19, 1, 3, remap=True)
+    for v in g.variants():
+        if v["kind"] != kind:
+            continue
+        steps = 2 * v["tb"] + 1
+        ref = base.copy()
+        oracle.naive_sweep(ref, steps)
+        st = to_problem(g, base)
+        g.run(st, steps, g.GpuConfig(tb=v["tb"], variant=v["index"]))
+        assert_state_equal(st, ref, f"variant {v}")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_minimum_grid(girih, oracle, kind):
+    # smallest admissible extents 2R+1 (stencil.cpp:61-63)
+    g = girih
+    R = TRAITS[kind][0]
+    m = 2 * R + 1
+    base = oracle.init_state(kind, m, m, m, 0, 1)
+    for tb in tbs_for(g, kind):
+        ref = base.copy()
+        oracle.naive_sweep(ref, 5)
+        st = to_problem(g, base)
+        g.run(st, 5, g.GpuConfig(tb=tb))
+        assert_state_equal(st, ref, f"min grid tb={tb}")
+
+
+def test_reference_golden_checksums_on_gpu(girih):
+    # proj/tests/test_stencil.cpp:145-153 through the device generator + device sweep
+    g = girih
+    s = g.init_state(g.VAR25PT, g.GridSpec(24, 24, 24, 0), 3)
+    g.run(s, 4)
+    assert g.interior_checksum(s) == 0x64179E6CB2CCF3DD
+    c = g.init_state(g.CONST7PT, g.GridSpec(16, 16, 16, 0), 11)
+    g.run(c, 5, g.GpuConfig(tb=4))
+    assert g.interior_checksum(c) == 0x99E588473D945C73
+
+
+def test_device_init_bitwise_equals_oracle_init(girih, oracle):
+    g = girih
+    for kind in range(4):
+        for remap in (False, True):
+            dims = (13, 12, 11, 3)
+            ds = g.init_state(kind, g.GridSpec(*dims), 42, remap=remap)
+            hs = oracle.init_state(kind, *dims, 42, remap=remap)
+            assert np.array_equal(ds.u.view(np.uint64), hs.u.view(np.uint64))
+            assert np.array_equal(ds.v.view(np.uint64), hs.v.view(np.uint64))
+            for a, b in zip(ds.coeffs, hs.coeffs):
+                assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+            assert np.array_equal(ds.cc.view(np.uint64), hs.cc.view(np.uint64))
+
+
+with open(os.path.join(HERE, "golden", "fixtures.json")) as f:
+    FIXTURES = json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", FIXTURES,
+                         ids=lambda c: f"k{c['kind']}-{c['nx']}x{c['ny']}x{c['nz']}-{c['engine']}")
+def test_gpu_reproduces_reference_fixtures(girih, oracle, case):
+    g = girih
+    hs = oracle.init_state(case["kind"], case["nx"], case["ny"], case["nz"], case["pad_x"],
+                           case["seed"], remap=case["remap"])
+    st = to_problem(g, hs)
+    for ch in case["chunks"]:
+        g.run(st, ch)
+    assert st.t_current == case["t_final"]
+    assert f"{oracle.fnv_all(st.u):#018x}" == case["fnv_u"]
+    assert f"{oracle.fnv_all(st.v):#018x}" == case["fnv_v"]
+    assert f"{g.interior_checksum(st):#018x}" == case["interior_checksum"]
+
+
+def test_zero_steps_is_noop_and_errors(girih, oracle):
+    # test_engine.cpp:159-168 and engine.cpp:335-337
+    g = girih
+    hs = oracle.init_state(0, 16, 16, 16, 0, 2)
+    st = to_problem(g, hs)
+    rep = g.run(st, 0)
+    assert rep.lups == 0 and rep.glups == 0.0
+    assert_state_equal(st, hs, "T=0")
+    with pytest.raises(ValueError):
+        g.run(st, -1)
+    bad = g.ProblemState(2, g.GridSpec(8, 8, 8, 0), st.u, st.v, [], st.cc, 0)
+    with pytest.raises(ValueError):
+        g.run(bad, 1)
+    with pytest.raises(ValueError):
+        g.run(st, 1, g.GpuConfig(tb=99))
+
+
+def test_device_state_stepwise_equals_single_run(girih, oracle):
+    g = girih
+    hs = oracle.init_state(1, 40, 40, 40, 0, 8, remap=True)
+    ref = hs.copy()
+    oracle.naive_sweep(ref, 13)
+    with g.DeviceState.from_state(to_problem(g, hs), g.GpuConfig(tb=4)) as ds:
+        for chunk in (1, 4, 8):
+            rep = ds.step(chunk)
+            assert rep.kernel_seconds > 0 and rep.n_launches >= 1
+        assert ds.t_current == 13
+        out = ds.download()
+    assert_state_equal(out, ref, "stepwise")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_emulated_z_slabs_bitwise(girih, oracle, kind):
+    # the multi-GPU z-slab decomposition (halo depth R*TBmax, exchange after every pass) run as
+    # several slabs on one device: must equal the single-domain oracle bitwise
+    g = girih
+    base = oracle.init_state(kind, 26, 21, 47, 1, 4, remap=True)
+    for nslab in (2, 3):
+        for tb in tbs_for(g, kind):
+            steps = 2 * tb + 3
+            ref = base.copy()
+            oracle.naive_sweep(ref, steps)
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb, emulate_slabs=nslab))
+            assert_state_equal(st, ref, f"slabs={nslab} tb={tb}")
+
+
+def test_inject_fault_is_detected(girih, oracle):
+    # main.cpp:137-140: a perturbed centre cell must make verify fail
+    g = girih
+    hs = oracle.init_state(0, 20, 20, 20, 0, 42)
+    ref = hs.copy()
+    oracle.naive_sweep(ref, 6)
+    st = to_problem(g, hs)
+    g.run(st, 6)
+    assert_state_equal(st, ref, "clean")
+    st.current()[1 + 10, 1 + 10, 1 + 10] += 1.0
+    with pytest.raises(AssertionError):
+        assert_state_equal(st, ref, "faulted")
+
+
+def test_tuner_restores_state(girih, oracle):
+    g = girih
+    hs = oracle.init_state(1, 64, 64, 64, 0, 1, remap=True)
+    with g.DeviceState.from_state(to_problem(g, hs)) as ds:
+        cfg, mlups, n = ds.tune(max_tb=4)
+        assert mlups > 0 and n >= 2 and 1 <= cfg.tb <= 4
+        assert ds.t_current == 0
+        out = ds.download()
+        assert_state_equal(out, hs, "state after tuning")
+        ds.set_config(cfg)
+        ds.step(5)
+        out = ds.download()
+    ref = hs.copy()
+    oracle.naive_sweep(ref, 5)
+    assert_state_equal(out, ref, "tuned run")
+
+
+@pytest.mark.slow
+def test_config1_full_size_bitwise(girih, oracle):
+    # BASELINE config 1 (const7pt 256^3, T=100) against the oracle at full size
+    g = girih
+    hs = oracle.init_state(0, 256, 256, 256, 0, 42, remap=True)
+    st = to_problem(g, hs)
+    g.run(st, 100)
+    oracle.naive_sweep(hs, 100)
+    assert g.interior_checksum(st) == 0x9F26250C918339D4
+    assert_state_equal(st, hs, "C1")
