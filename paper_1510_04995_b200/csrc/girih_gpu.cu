@@ -641,8 +641,12 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
                         long long t0, LaunchInfo* li) {
     Slab& s = h.slabs[slab_index];
     const int R = h.R, H = ps.tb * R;
-    const int OX = var->lx - 2 * H, OY = var->ly - 2 * H;
+    // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
+    const int hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
+    const int OX = var->lx - 2 * hx, OY = var->ly - 2 * H;
     PassParams p{};
+    p.hx = hx;
+    p.ox = OX;
     p.src_prev = ps.src_prev >= 0 ? s.buf[ps.src_prev]->p : nullptr;
     p.dst_final = s.buf[ps.dst]->p;
     p.dst_penult = ps.dst_penult >= 0 ? s.buf[ps.dst_penult]->p : nullptr;
@@ -682,7 +686,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     // nzl + 2 nzc (TB-s) R planes
     li->computed_lups = 0;
     for (int lev = 1; lev <= ps.tb; ++lev) {
-        const long long ex = (long long)(OX + 2 * (ps.tb - lev) * R);
+        const long long ex = (long long)(OX + 2 * (hx - lev * R));
         const long long ey = (long long)(OY + 2 * (ps.tb - lev) * R);
         const long long ez = (long long)nzl + 2LL * p.nzc * (ps.tb - lev) * R;
         li->computed_lups += ex * ey * (long long)txy * ez;

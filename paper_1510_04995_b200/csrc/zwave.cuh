@@ -14,7 +14,8 @@
 //     newest plane (k_s+R) from the register the same thread produced one level earlier;
 //   * levels 1..TB-1 are kept in per-level rings of 2R+1 planes; level TB is stored to HBM;
 //   * the tile shrinks by R per side per level (overlapped / trapezoid tiling in x and y,
-//     and in z at z-chunk boundaries), so no inter-CTA synchronisation exists inside a pass.
+//     and in z at z-chunk boundaries), so no inter-CTA synchronisation exists inside a pass;
+//     the x halo is H or H+1 so that every TMA box starts on a 16-byte boundary.
 //
 // One __syncthreads per z-plane orders every cross-thread smem dependency: all values a
 // level reads from smem were produced at least one iteration earlier.
@@ -61,6 +62,8 @@ struct PassParams {
     int nzc, zc_len;         // z chunks per tile column and output planes per chunk
     int zout_lo, zout_hi;    // local output planes [lo, hi)
     int units;               // tiles_x * tiles_y * nzc
+    int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
+                             // innermost box coordinate 16-byte aligned (even for fp64)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -133,7 +136,7 @@ struct ZwaveConfig {
     static constexpr int NRING = NR0 + (TB - 1) * Q;
     static constexpr size_t SMEM = size_t(NRING) * CELLS * sizeof(double) + NR0 * sizeof(uint64_t);
     static_assert(CELLS % NT == 0, "tile must split evenly over the CTA");
-    static_assert(OX > 0 && OY > 0, "tile too small for the halo");
+    static_assert(OX - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
     static_assert((LX * 8) % 16 == 0, "TMA inner box must be a multiple of 16 bytes");
 };
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(NT, 1)
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P>;
     constexpr int R = CFG::R, Q = CFG::Q, NR0 = CFG::NR0, H = CFG::H;
     constexpr int CELLS = CFG::CELLS, CPT = CFG::CPT;
-    constexpr int OX = CFG::OX, OY = CFG::OY;
+    constexpr int OY = CFG::OY;
     constexpr uint32_t PLANE_BYTES = CELLS * sizeof(double);
     // large multiples keep ring indices non-negative for planes below 0
     constexpr int KOFF = Q * 4096;
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (pu >= p.units) return;
         const int j = pg.za - H + pit;
         const int slot = int(pgidx % NR0);
-        const int xd = p.off + pg.tx * OX + R - H;
+        const int xd = p.off + pg.tx * p.ox + R - p.hx;  // even by construction
         const int yd = pg.ty * OY + R - H;
         mbar_arrive_expect_tx(&mbar[slot], PLANE_BYTES);
         tma_load_plane(ring0 + slot * CELLS, &src_map, xd, yd, j, &mbar[slot]);
@@ -196,19 +199,22 @@ __global__ void __launch_bounds__(NT, 1)
 
     // ---- per-thread cell constants ----
     int lcell[CPT], dmin[CPT];
+    bool out_col[CPT];
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
         const int c = tid + NT * i;
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
-        dmin[i] = min(min(lx, LX - 1 - lx), min(ly, LY - 1 - ly));
+        const int dx = min(lx, LX - 1 - lx), dy = min(ly, LY - 1 - ly);
+        dmin[i] = min(dx, dy);
+        out_col[i] = dx >= p.hx && dy >= H;
     }
 
     long long g = G0;  // consumer's global element index
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const UnitGeom ug = unit_geom(p, u);
         const int n_it = (ug.zb - ug.za) + 2 * H;
-        const int xa0 = ug.tx * OX + R - H;  // allocated x of local lx = 0
+        const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
         const int ya0 = ug.ty * OY + R - H;
 
         // per-cell column data for this unit
@@ -242,9 +248,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
                 for (int s = 1; s <= TB; ++s) {
                     const int k = j - s * R;  // plane of level s
-                    if (it < 2 * s * R || k < 0 || k >= p.Zloc) break;  // uniform
+                    // lower bounds are monotone in s (higher levels sit on lower planes)
+                    if (it < 2 * s * R || k < 0) break;  // uniform
                     if (dmin[i] < s * R) break;  // column outside level-s valid area
                     if (!col_alloc[i]) break;
+                    // above the buffer: skip this level only; level s+1 sits R planes lower
+                    // (a ghost plane there, so it never reads this level's value)
+                    if (k >= p.Zloc) continue;
                     const int kg = k + p.zoff;
                     const bool plane_ghost = kg < R || kg >= R + p.nzg;
                     const long long gidx = (long long)k * p.plane + colidx[i];
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(NT, 1)
                         newest = val;
                     } else {
                         // level TB: output tile cells of interior planes [za, zb)
-                        if (dmin[i] >= H && !col_ghost[i] && k >= ug.za && k < ug.zb) {
+                        if (out_col[i] && !col_ghost[i] && k >= ug.za && k < ug.zb) {
                             p.dst_final[gidx] = val;
                             if (p.dst_penult) p.dst_penult[gidx] = V(0, 0, 0);
                         }

@@ -224,8 +224,7 @@ def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     lib = load()
     addr = p.value
     weakref.finalize(buf, lambda: lib.girih_gpu_host_free(C.c_void_p(addr)))
-    arr._pinned_owner = buf  # noqa: SLF001 -- keep the allocation alive with the array
-    return arr
+    return arr  # arr.base -> buf keeps the page-locked allocation alive
 
 
 class DeviceState:
