@@ -80,8 +80,8 @@ struct KindInfo {
     int default_tb;
 };
 const KindInfo kKinds[4] = {
-    {"const7pt", 1, 2, 7, 1, 0, 16, 10, 4},
-    {"var7pt", 1, 9, 13, 1, 7, 72, 13, 4},
+    {"const7pt", 1, 2, 7, 1, 0, 16, 10, 2},
+    {"var7pt", 1, 9, 13, 1, 7, 72, 13, 2},
     {"const25pt", 4, 3, 33, 2, 1, 32, 33, 1},
     {"var25pt", 4, 15, 37, 1, 13, 120, 37, 1},
 };
@@ -312,18 +312,23 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-CUtensorMap make_plane_map(const double* base, int pitch, int Y, int Zloc, int lx, int ly) {
+// fp64 tiled map: 3-D (x, y, z) over dims {dx, dy, dz}, or 4-D (x, y, z, array) when narr > 1;
+// row pitch / plane / array strides in elements; box bx x by x 1 (x narr)
+CUtensorMap make_map(const double* base, long long dx, long long dy, long long dz, int narr,
+                     long long row, long long plane, long long arr, int bx, int by) {
     CUtensorMap map;
-    cuuint64_t dims[3] = {cuuint64_t(pitch), cuuint64_t(Y), cuuint64_t(Zloc)};
-    cuuint64_t strides[2] = {cuuint64_t(pitch) * 8, cuuint64_t(pitch) * Y * 8};
-    cuuint32_t box[3] = {cuuint32_t(lx), cuuint32_t(ly), 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = get_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+    const cuuint32_t rank = narr > 1 ? 4 : 3;
+    cuuint64_t dims[4] = {cuuint64_t(dx), cuuint64_t(dy), cuuint64_t(dz), cuuint64_t(narr)};
+    cuuint64_t strides[3] = {cuuint64_t(row) * 8, cuuint64_t(plane) * 8, cuuint64_t(arr) * 8};
+    cuuint32_t box[4] = {cuuint32_t(bx), cuuint32_t(by), 1, cuuint32_t(narr)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = get_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
                                  const_cast<double*>(base), dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    if (r != CUDA_SUCCESS)
+        throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
 }
 
@@ -352,7 +357,8 @@ struct Slab {
     int Zloc = 0, zoff = 0;
     int zout_lo = 0, zout_hi = 0;  // own interior planes (local)
     std::unique_ptr<DevBuf> buf[4];     // u, v, scratch even, scratch odd
-    std::vector<std::unique_ptr<DevBuf>> coeff;
+    std::unique_ptr<DevBuf> cblock;     // coefficient fields, contiguous [c][k][j][i]
+    double* coeff(int c, size_t slab_elems) const { return cblock->p + size_t(c) * slab_elems; }
     cudaEvent_t done = nullptr;    // end of this slab's work in the current pass
 };
 
@@ -370,13 +376,13 @@ struct Handle {
     int sm_count = 0;
     // timing events (slab 0 stream)
     std::vector<cudaEvent_t> ev;
-    // cached tensor maps: key (slab, buffer, lx, ly)
+    // cached tensor maps: key (base pointer, arrays, box, interior flag)
     struct MapEntry {
-        int slab, buf, lx, ly;
         const double* base;
+        int narr, bx, by, interior;
         CUtensorMap map;
     };
-    std::vector<MapEntry> maps;
+    std::vector<std::unique_ptr<MapEntry>> maps;
 
     size_t plane_elems() const { return size_t(pitch) * Y; }
     size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
@@ -467,8 +473,7 @@ void setup_slabs(Handle& h) {
         const size_t n = h.slab_elems(s);
         alloc_buf(s.buf[0], s.device, n, s.stream);
         alloc_buf(s.buf[1], s.device, n, s.stream);
-        s.coeff.resize(h.nc);
-        for (int c = 0; c < h.nc; ++c) alloc_buf(s.coeff[c], s.device, n, s.stream);
+        if (h.nc > 0) alloc_buf(s.cblock, s.device, n * h.nc, s.stream);
     }
     if (!h.emulated && nslab > 1) {
         for (int g = 0; g + 1 < nslab; ++g) {
@@ -557,7 +562,7 @@ void upload_state(Handle& h, const girih_state_view& v) {
         copy_h2d(h, d.data(), f == 0 ? v.u : v.v);
     }
     for (int c = 0; c < h.nc; ++c) {
-        for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].coeff[c]->p;
+        for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].coeff(c, h.slab_elems(h.slabs[g]));
         copy_h2d(h, d.data(), v.coeffs[c]);
     }
     std::memcpy(h.cc, v.cc, sizeof h.cc);
@@ -584,7 +589,7 @@ void init_state_device(Handle& h, uint64_t seed, int remap) {
             GCHECK(launch_init_field(s.buf[f]->p, h.pitch, h.off, h.X, h.Y, s.Zloc, s.zoff, h.Z,
                                      seed, f, remap, 1.0, s.stream));
         for (int c = 0; c < ki.ncoeff; ++c)
-            GCHECK(launch_init_field(s.coeff[c]->p, h.pitch, h.off, h.X, h.Y, s.Zloc, s.zoff, h.Z,
+            GCHECK(launch_init_field(s.coeff(c, h.slab_elems(s)), h.pitch, h.off, h.X, h.Y, s.Zloc, s.zoff, h.Z,
                                      seed, 2 + c, remap, coeff_scale, s.stream));
     }
     for (int c = 0; c < 5; ++c) h.cc[c] = init_value_h(seed, 64, 0, 0, c);
@@ -604,13 +609,31 @@ void init_state_device(Handle& h, uint64_t seed, int remap) {
     sync_all(h);
 }
 
-const CUtensorMap& plane_map(Handle& h, int slab, int buf, int lx, int ly) {
-    const double* base = h.slabs[slab].buf[buf]->p;
+// Load maps cover a whole slab buffer (device rows incl. padding); the store map (interior = 1)
+// covers only the slab's own interior cells, so TMA stores clip at the domain boundary and
+// never touch ghost or pad cells.
+const CUtensorMap& tensor_map(Handle& h, int slab, const double* base, int narr, int bx, int by,
+                              int interior = 0) {
     for (auto& m : h.maps)
-        if (m.slab == slab && m.buf == buf && m.lx == lx && m.ly == ly && m.base == base) return m.map;
-    h.maps.push_back({slab, buf, lx, ly, base,
-                      make_plane_map(base, h.pitch, h.Y, h.slabs[slab].Zloc, lx, ly)});
-    return h.maps.back().map;
+        if (m->base == base && m->narr == narr && m->bx == bx && m->by == by &&
+            m->interior == interior)
+            return m->map;
+    auto e = std::make_unique<Handle::MapEntry>();
+    e->base = base;
+    e->narr = narr;
+    e->bx = bx;
+    e->by = by;
+    e->interior = interior;
+    const Slab& s = h.slabs[slab];
+    const long long plane = h.plane_elems();
+    if (interior) {
+        const double* b0 = base + (size_t)s.zout_lo * plane + (size_t)h.R * h.pitch + h.off + h.R;
+        e->map = make_map(b0, h.nx, h.ny, s.zout_hi - s.zout_lo, 1, h.pitch, plane, 0, bx, by);
+    } else {
+        e->map = make_map(base, h.pitch, h.Y, s.Zloc, narr, h.pitch, plane, plane * s.Zloc, bx, by);
+    }
+    h.maps.push_back(std::move(e));
+    return h.maps.back()->map;
 }
 
 // z chunks per tile column: minimise (waves of units) x (planes streamed per unit)
@@ -652,7 +675,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.dst_penult = ps.dst_penult >= 0 ? s.buf[ps.dst_penult]->p : nullptr;
     p.ghost[0] = s.buf[0]->p;
     p.ghost[1] = s.buf[1]->p;
-    for (int c = 0; c < h.nc; ++c) p.coeff[c] = s.coeff[c]->p;
+    for (int c = 0; c < h.nc; ++c) p.coeff[c] = s.coeff(c, h.slab_elems(s));
     for (int c = 0; c < 5; ++c) p.cc[c] = h.cc[c];
     p.parity0 = parity_of(t0);
     p.nx = h.nx;
@@ -763,9 +786,18 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             GCHECK(cudaSetDevice(s.device));
             LaunchInfo li;
             const PassParams p = build_params(h, ps, var, int(g), t, &li);
-            const CUtensorMap& map = plane_map(h, int(g), ps.src, var->lx, var->ly);
+            const CUtensorMap& vmap = tensor_map(h, int(g), s.buf[ps.src]->p, 1, var->lx, var->ly);
+            const CUtensorMap* cmap = &vmap;
+            const CUtensorMap* umap = &vmap;
+            if (h.nc > 0)
+                cmap = &tensor_map(h, int(g), s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc,
+                                   var->aux_x, var->aux_y);
+            if (ps.src_prev >= 0)
+                umap = &tensor_map(h, int(g), s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
+            const CUtensorMap& omap = tensor_map(h, int(g), s.buf[ps.dst]->p, 1, p.ox,
+                                                 var->ly - 2 * ps.tb * h.R, 1);
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi], s.stream));
-            GCHECK(var->launch(map, p, li.grid, s.stream));
+            GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi + 1], s.stream));
             st.computed += li.computed_lups;
             st.grid = li.grid;
@@ -819,7 +851,7 @@ void destroy(Handle* h) {
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
     for (Slab& s : h->slabs) {
         for (auto& b : s.buf) b.reset();
-        s.coeff.clear();
+        s.cblock.reset();
         if (s.own_stream && s.stream) {
             cudaSetDevice(s.device);
             cudaStreamDestroy(s.stream);
@@ -1007,7 +1039,8 @@ int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double
         std::vector<double*> d(h.slabs.size());
         for (int c = 0; c < n; ++c) {
             if (!coeffs || !coeffs[c]) continue;
-            for (size_t g = 0; g < h.slabs.size(); ++g) d[g] = h.slabs[g].coeff[c]->p;
+            for (size_t g = 0; g < h.slabs.size(); ++g)
+                d[g] = h.slabs[g].coeff(c, h.slab_elems(h.slabs[g]));
             copy_d2h(h, d.data(), coeffs[c]);
         }
         sync_all(h);

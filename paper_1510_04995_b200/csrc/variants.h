@@ -8,13 +8,15 @@
 
 namespace girih_gpu {
 
-using LaunchFn = cudaError_t (*)(const CUtensorMap& map, const PassParams& p, int grid,
-                                 cudaStream_t stream);
+using LaunchFn = cudaError_t (*)(const CUtensorMap& vmap, const CUtensorMap& cmap,
+                                 const CUtensorMap& umap, const CUtensorMap& omap,
+                                 const PassParams& p, int grid, cudaStream_t stream);
 using OccFn = cudaError_t (*)(int* blocks_per_sm);
 
 struct Variant {
-    int kind, tb, lx, ly, threads, prefetch;
+    int kind, tb, lx, ly, threads, prefetch, aux_prefetch, min_blocks;
     int smem_bytes;
+    int aux_x0, aux_y0, aux_x, aux_y;  // coefficient (aux) box inside the tile
     LaunchFn launch;
     OccFn occupancy;
 };
@@ -29,11 +31,12 @@ extern const int kNumVariantsConst25;
 extern const Variant kVariantsVar25[];
 extern const int kNumVariantsVar25;
 
-template <int KIND, int TB, int LX, int LY, int NT, int P>
-cudaError_t launch_zwave(const CUtensorMap& map, const PassParams& p, int grid,
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
+cudaError_t launch_zwave(const CUtensorMap& vmap, const CUtensorMap& cmap, const CUtensorMap& umap,
+                         const CUtensorMap& omap, const PassParams& p, int grid,
                          cudaStream_t stream) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -41,24 +44,29 @@ cudaError_t launch_zwave(const CUtensorMap& map, const PassParams& p, int grid,
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    fn<<<grid, NT, CFG::SMEM, stream>>>(map, p);
+    fn<<<grid, NT, CFG::SMEM, stream>>>(vmap, cmap, umap, omap, p);
     return cudaGetLastError();
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
 cudaError_t occupancy_zwave(int* blocks) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB>;
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, NT, CFG::SMEM);
 }
 
-#define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P)                                              \
-    Variant {                                                                                \
-        KIND, TB, LX, LY, NT, P, int(ZwaveConfig<KIND, TB, LX, LY, NT, P>::SMEM),          \
-            &launch_zwave<KIND, TB, LX, LY, NT, P>, &occupancy_zwave<KIND, TB, LX, LY, NT, P> \
+#define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB)                                        \
+    Variant {                                                                                 \
+        KIND, TB, LX, LY, NT, P, PA, MINB, int(ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::SMEM),     \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AXO,                                    \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AYO,                                    \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AX,                                     \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AY,                                     \
+            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>,                                       \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>                                     \
     }
 
 }  // namespace girih_gpu

@@ -1,11 +1,14 @@
+// Best-first within each fused depth: select_variant() takes the first match.
 // variants_const25.cu -- zwave instantiations for const25 (kept in its own TU so nvcc builds kinds in parallel).
 #include "variants.h"
 
 namespace girih_gpu {
 
 const Variant kVariantsConst25[] = {
-    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 512, 2),
-    GIRIH_VARIANT(K_CONST25, 2, 32, 32, 256, 2),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 16, 256, 1, 1, 2),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 24, 384, 2, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 1, 32, 32, 256, 2, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 2, 32, 32, 256, 2, 1, 1),
 };
 const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
 

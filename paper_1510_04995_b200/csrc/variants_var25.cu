@@ -1,11 +1,12 @@
+// Best-first within each fused depth: select_variant() takes the first match.
 // variants_var25.cu -- zwave instantiations for var25 (kept in its own TU so nvcc builds kinds in parallel).
 #include "variants.h"
 
 namespace girih_gpu {
 
 const Variant kVariantsVar25[] = {
-    GIRIH_VARIANT(K_VAR25, 1, 64, 32, 512, 2),
-    GIRIH_VARIANT(K_VAR25, 2, 32, 32, 256, 2),
+    GIRIH_VARIANT(K_VAR25, 1, 32, 16, 128, 1, 1, 2),
+    GIRIH_VARIANT(K_VAR25, 1, 32, 32, 256, 2, 1, 1),
 };
 const int kNumVariantsVar25 = sizeof(kVariantsVar25) / sizeof(kVariantsVar25[0]);
 

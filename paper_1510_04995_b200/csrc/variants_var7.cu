@@ -1,13 +1,17 @@
+// Best-first within each fused depth: select_variant() takes the first match.
 // variants_var7.cu -- zwave instantiations for var7 (kept in its own TU so nvcc builds kinds in parallel).
 #include "variants.h"
 
 namespace girih_gpu {
 
 const Variant kVariantsVar7[] = {
-    GIRIH_VARIANT(K_VAR7, 1, 64, 32, 512, 2),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 32, 512, 2),
-    GIRIH_VARIANT(K_VAR7, 3, 64, 32, 512, 2),
-    GIRIH_VARIANT(K_VAR7, 4, 64, 32, 512, 2),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 8, 256, 3, 1, 2),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 16, 256, 4, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 1, 32, 16, 256, 3, 1, 2),
+    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 256, 2, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 32, 16, 256, 2, 1, 2),
+    GIRIH_VARIANT(K_VAR7, 3, 32, 16, 256, 3, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 4, 32, 16, 256, 2, 1, 1),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

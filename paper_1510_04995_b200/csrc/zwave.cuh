@@ -9,6 +9,11 @@
 //   * level 0 (the input time level) arrives plane by plane by TMA (cp.async.bulk.tensor,
 //     box LX x LY x 1) into a ring of NR0 = 2R+1+P planes completed on mbarriers, P planes
 //     ahead of use -- the z-wavefront;
+//   * the time-invariant coefficient fields (one contiguous [c][k][j][i] block) arrive by ONE
+//     4-D TMA per plane (box AX x AY x 1 x NC, the level-1 area) into an aux ring deep enough
+//     that level s re-uses the plane level 1 fetched (s-1)*R iterations earlier -- each
+//     coefficient byte crosses HBM once per pass, not once per fused step; const25pt's
+//     level t0-1 field rides in the same aux ring;
 //   * level s (1..TB) of plane k_s = j - s*R is computed at global iteration j from level
 //     s-1 planes k_s-R .. k_s+R: x/y/z neighbours come from the level-(s-1) smem ring, the
 //     newest plane (k_s+R) from the register the same thread produced one level earlier;
@@ -66,6 +71,8 @@ struct PassParams {
                              // innermost box coordinate 16-byte aligned (even for fp64)
 };
 
+
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -102,11 +109,42 @@ __device__ __forceinline__ void tma_load_plane(void* dst, const CUtensorMap* map
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            int w, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// bulk tensor store smem -> global (async proxy) and its bulk-group bookkeeping
+__device__ __forceinline__ void tma_store_plane(const CUtensorMap* map, const void* src, int x, int y,
+                                                int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-// Work-unit cursor: unit u -> (tile x, tile y, z chunk); a unit's level-0 stream covers
+// Work-unit geometry: unit u -> (tile x, tile y, z chunk); a unit's level-0 stream covers
 // planes [za - H, zb + H).
 struct UnitGeom {
     int tx, ty, za, zb;
@@ -123,177 +161,261 @@ __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
     return g;
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P>
+// Producer cursor over the CTA's persistent unit list (static round robin over units).
+struct Cursor {
+    int u, it, n_it;
+    UnitGeom ug;
+};
+
+template <int H>
+__device__ __forceinline__ void cursor_init(Cursor& c, const PassParams& p) {
+    c.u = blockIdx.x;
+    c.it = 0;
+    c.n_it = 0;
+    if (c.u < p.units) {
+        c.ug = unit_geom(p, c.u);
+        c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
+    }
+}
+
+template <int H>
+__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p) {
+    if (++c.it >= c.n_it) {
+        c.it = 0;
+        c.u += gridDim.x;
+        if (c.u < p.units) {
+            c.ug = unit_geom(p, c.u);
+            c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
+        }
+    }
+}
+
+template <int KIND> struct AuxArrays { static constexpr int N = KindTraits<KIND>::NC; };
+template <> struct AuxArrays<K_CONST25> { static constexpr int N = 2; };  // C and level t0-1
+
+constexpr int round16(int n) { return (n + 15) / 16 * 16; }
+
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1>
 struct ZwaveConfig {
     static constexpr int R = KindTraits<KIND>::R;
     static constexpr int Q = 2 * R + 1;     // z window of one level
     static constexpr int NR0 = Q + P;       // level-0 TMA ring depth
     static constexpr int H = TB * R;        // halo of the loaded tile
-    static constexpr int OX = LX - 2 * H;   // output tile
-    static constexpr int OY = LY - 2 * H;
+    static constexpr int OY = LY - 2 * H;   // output tile height (x: runtime, halo H or H+1)
+    static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
     static constexpr int CPT = CELLS / NT;  // cells per thread
     static constexpr int NRING = NR0 + (TB - 1) * Q;
-    static constexpr size_t SMEM = size_t(NRING) * CELLS * sizeof(double) + NR0 * sizeof(uint64_t);
+    // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
+    static constexpr int NAUX = AuxArrays<KIND>::N;
+    static constexpr int AXO = R & ~1, AYO = R;
+    static constexpr int AX = LX - 2 * AXO, AY = LY - 2 * AYO;
+    static constexpr int AYX = AX * AY;
+    static constexpr int NAR = NAUX > 0 ? (TB - 1) * R + 1 + PA : 0;  // aux ring depth
+    static constexpr int AUXPLANE = NAUX * AYX;
+    // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
+    static constexpr int GUARD = round16(LX * R + R);
+    static constexpr int STAGE = round16(OXM * OY);  // one output staging plane
+    static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
+                                           size_t(NAR) * AUXPLANE + 2 * size_t(STAGE);
+    static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
     static_assert(CELLS % NT == 0, "tile must split evenly over the CTA");
-    static_assert(OX - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
+    static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
+    static_assert(LX - 2 * H - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
-    static_assert((LX * 8) % 16 == 0, "TMA inner box must be a multiple of 16 bytes");
+    static_assert((LX * 8) % 16 == 0 && (AX * 8) % 16 == 0, "TMA inner box must be 16-byte multiple");
+    static_assert((CELLS * 8) % 128 == 0 && (AYX * 8) % 128 == 0, "TMA smem boxes 128-byte aligned");
+    static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
-template <int KIND, int TB, int LX, int LY, int NT, int P>
-__global__ void __launch_bounds__(NT, 1)
-    zwave_kernel(const __grid_constant__ CUtensorMap src_map,
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    zwave_kernel(const __grid_constant__ CUtensorMap vmap,  // level-0 source buffer (3-D)
+                 const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
+                 const __grid_constant__ CUtensorMap umap,  // const25pt: level t0-1 (3-D)
+                 const __grid_constant__ CUtensorMap omap,  // output: interior of dst_final
                  const __grid_constant__ PassParams p) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
     constexpr int R = CFG::R, Q = CFG::Q, NR0 = CFG::NR0, H = CFG::H;
-    constexpr int CELLS = CFG::CELLS, CPT = CFG::CPT;
-    constexpr int OY = CFG::OY;
+    constexpr int CELLS = CFG::CELLS, CPT = CFG::CPT, OY = CFG::OY;
+    constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
+    constexpr int AX = CFG::AX, AYX = CFG::AYX, AUXPLANE = CFG::AUXPLANE;
+    constexpr int GUARD = CFG::GUARD, STAGE = CFG::STAGE;
     constexpr uint32_t PLANE_BYTES = CELLS * sizeof(double);
-    // large multiples keep ring indices non-negative for planes below 0
-    constexpr int KOFF = Q * 4096;
+    constexpr uint32_t AUX_BYTES = AUXPLANE * sizeof(double);
+    constexpr int KOFF = Q * 4096;  // keeps ring indices of planes below 0 non-negative
+    // stream counters start at a common multiple of the ring depths (first phase parity 0)
+    constexpr uint32_t G0 = 8u * NR0 * (NAR > 0 ? NAR : 1);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring0 = reinterpret_cast<double*>(smem_raw);
-    double* ringL = ring0 + NR0 * CELLS;  // level s (1..TB-1) ring at ringL + (s-1)*Q*CELLS
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(ringL + (TB - 1) * Q * CELLS);
+    double* ring0 = reinterpret_cast<double*>(smem_raw) + GUARD;
+    double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*Q*CELLS
+    double* auxr = ringL + (TB - 1) * Q * CELLS;   // aux planes: NAR x [NAUX][AY][AX]
+    double* stage = auxr + NAR * AUXPLANE + GUARD; // 2 output staging planes [OY][ox]
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 2 * STAGE);
+    uint64_t* abar = vbar + NR0;
 
     const int tid = threadIdx.x;
     if (tid == 0) {
-        for (int b = 0; b < NR0; ++b) mbar_init(&mbar[b], 1);
+        for (int b = 0; b < NR0; ++b) mbar_init(&vbar[b], 1);
+        for (int b = 0; b < NAR; ++b) mbar_init(&abar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fence_proxy_async_smem();
     }
     __syncthreads();
 
-    // ---- producer cursor (thread 0): element index g -> (unit, iteration) ----
-    // Global stream counter starts at a multiple of NR0 so that early (g - 2R) indices stay
-    // non-negative and the first phase parity is 0.
-    constexpr long long G0 = 4LL * NR0;
-    int pu = blockIdx.x;          // producer's unit
-    int pit = 0;                  // producer's iteration within the unit
-    UnitGeom pg{};
-    if (pu < p.units) pg = unit_geom(p, pu);
-    long long pgidx = G0;         // global index of the next element to load
-
-    auto producer_issue = [&](void) {
-        // issue the load for element pgidx, then advance the cursor
-        if (pu >= p.units) return;
-        const int j = pg.za - H + pit;
-        const int slot = int(pgidx % NR0);
-        const int xd = p.off + pg.tx * p.ox + R - p.hx;  // even by construction
-        const int yd = pg.ty * OY + R - H;
-        mbar_arrive_expect_tx(&mbar[slot], PLANE_BYTES);
-        tma_load_plane(ring0 + slot * CELLS, &src_map, xd, yd, j, &mbar[slot]);
-        ++pgidx;
-        ++pit;
-        if (pit >= (pg.zb - pg.za) + 2 * H) {
-            pit = 0;
-            pu += gridDim.x;
-            if (pu < p.units) pg = unit_geom(p, pu);
+    // ---- producers (thread 0): V runs P elements ahead, aux PA elements ahead ----
+    Cursor vcur{}, acur{};
+    uint32_t vnext = G0, anext = G0;
+    auto issue_v = [&]() {
+        if (vcur.u >= p.units) return;
+        const int j = vcur.ug.za - H + vcur.it;
+        const int slot = int(vnext % NR0);
+        const int xd = p.off + vcur.ug.tx * p.ox + R - p.hx;  // even by construction
+        const int yd = vcur.ug.ty * OY + R - H;
+        mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
+        tma_load_plane(ring0 + slot * CELLS, &vmap, xd, yd, j, &vbar[slot]);
+        ++vnext;
+        cursor_next<H>(vcur, p);
+    };
+    auto issue_a = [&]() {
+        if constexpr (NAUX > 0) {
+            if (acur.u >= p.units) return;
+            const int k1 = acur.ug.za - H + acur.it - R;  // level-1 plane of that iteration
+            const int slot = int(anext % NAR);
+            const int xd = p.off + acur.ug.tx * p.ox + R - p.hx + AXO;
+            const int yd = acur.ug.ty * OY + R - H + AYO;
+            mbar_arrive_expect_tx(&abar[slot], AUX_BYTES);
+            double* dst = auxr + slot * AUXPLANE;
+            if constexpr (KIND == K_CONST25) {
+                tma_load_plane(dst, &cmap, xd, yd, k1, &abar[slot]);
+                tma_load_plane(dst + AYX, &umap, xd, yd, k1, &abar[slot]);
+            } else {
+                tma_load_4d(dst, &cmap, xd, yd, k1, 0, &abar[slot]);
+            }
+            ++anext;
+            cursor_next<H>(acur, p);
         }
     };
+    if (tid == 0) {
+        cursor_init<H>(vcur, p);
+        cursor_init<H>(acur, p);
+        for (int e = 0; e < P; ++e) issue_v();
+        for (int e = 0; e < PA; ++e) issue_a();
+    }
+    // output store pending from the previous iteration (thread 0)
+    bool pend = false;
+    int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0;
 
-    if (tid == 0)
-        for (int e = 0; e < P; ++e) producer_issue();
-
-    // ---- per-thread cell constants ----
-    int lcell[CPT], dmin[CPT];
-    bool out_col[CPT];
+    // ---- per-thread cell constants (bit i of a mask = cell i of this thread) ----
+    int lcell[CPT], dyv[CPT], ai[CPT], sidx[CPT];
+    uint32_t out_mask = 0;
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
         const int c = tid + NT * i;
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
         const int dx = min(lx, LX - 1 - lx), dy = min(ly, LY - 1 - ly);
-        dmin[i] = min(dx, dy);
-        out_col[i] = dx >= p.hx && dy >= H;
+        dyv[i] = dy;  // warp-uniform (a warp covers part of one tile row)
+        if (dx >= p.hx && dy >= H) out_mask |= 1u << i;
+        ai[i] = (ly - AYO) * AX + (lx - AXO);
+        sidx[i] = (ly - H) * p.ox + (lx - p.hx);
     }
+    const bool has_penult = p.dst_penult != nullptr;
 
-    long long g = G0;  // consumer's global element index
+    uint32_t g = G0;  // consumer's global element index
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const UnitGeom ug = unit_geom(p, u);
         const int n_it = (ug.zb - ug.za) + 2 * H;
         const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
         const int ya0 = ug.ty * OY + R - H;
 
-        // per-cell column data for this unit
-        int xa[CPT], ya[CPT];
-        bool col_alloc[CPT], col_ghost[CPT];
-        long long colidx[CPT];
+        // ghost columns (ghost value instead of the stencil) and in-allocation columns
+        uint32_t ghost_mask = 0, ok_mask = 0;
+        int colidx[CPT];  // row offset within a plane (allocated coordinates)
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-            const int lx = lcell[i] % LX, ly = lcell[i] / LX;
-            xa[i] = xa0 + lx;
-            ya[i] = ya0 + ly;
-            col_alloc[i] = xa[i] >= 0 && xa[i] < p.X && ya[i] >= 0 && ya[i] < p.Y;
-            col_ghost[i] = xa[i] < R || xa[i] >= R + p.nx || ya[i] < R || ya[i] >= R + p.ny;
-            const int cx = min(max(xa[i], 0), p.X - 1), cy = min(max(ya[i], 0), p.Y - 1);
-            colidx[i] = (long long)cy * p.pitch + p.off + cx;
+            const int xa = xa0 + lcell[i] % LX, ya = ya0 + lcell[i] / LX;
+            if (xa >= 0 && xa < p.X && ya >= 0 && ya < p.Y) ok_mask |= 1u << i;
+            if (xa < R || xa >= R + p.nx || ya < R || ya >= R + p.ny) ghost_mask |= 1u << i;
+            const int cx = min(max(xa, 0), p.X - 1), cy = min(max(ya, 0), p.Y - 1);
+            colidx[i] = cy * p.pitch + p.off + cx;
         }
+        const uint32_t col_fix = ghost_mask & ok_mask;
+        const bool any_ghost_col = __syncthreads_or(col_fix != 0);
 
         for (int it = 0; it < n_it; ++it, ++g) {
             const int j = ug.za - H + it;  // level-0 plane of this iteration
-            __syncthreads();               // previous iteration's smem traffic is complete
-            if (tid == 0) producer_issue();
-            {
-                const int slot = int(g % NR0);
-                mbar_wait(&mbar[slot], uint32_t((g / NR0) & 1));
+            __syncthreads();               // previous iteration's smem reads/writes are complete
+            if (tid == 0) {
+                if (pend) {  // output plane of the previous iteration (staging fenced by writers)
+                    tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
+                    bulk_commit();
+                    pend = false;
+                }
+                issue_v();
+                issue_a();
             }
+            mbar_wait(&vbar[g % NR0], (g / NR0) & 1);
+            if constexpr (NAUX > 0) mbar_wait(&abar[g % NAR], (g / NAR) & 1);
 
-            // uniform per-level plane data
+            double newest[CPT];  // level s-1 at (cell, k_s + R), produced this iteration
+            bool staged = false;
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) {
-                double newest = 0.0;  // level s-1 value at (cell, k_s + R)
+            for (int s = 1; s <= TB; ++s) {
+                const int k = j - s * R;  // plane of level s
+                // lower bounds are monotone in s (higher levels sit on lower planes)
+                if (it < 2 * s * R || k < 0) break;
+                // above the buffer: skip this level only; level s+1 sits R planes lower (a
+                // ghost plane there, so it never reads this level's value)
+                if (k >= p.Zloc) continue;
+                const int kg = k + p.zoff;
+                const bool plane_ghost = kg < R || kg >= R + p.nzg;
+                const double* pl[Q];  // level s-1 planes k-R .. k+R
+                if (s == 1) {
 #pragma unroll
-                for (int s = 1; s <= TB; ++s) {
-                    const int k = j - s * R;  // plane of level s
-                    // lower bounds are monotone in s (higher levels sit on lower planes)
-                    if (it < 2 * s * R || k < 0) break;  // uniform
-                    if (dmin[i] < s * R) break;  // column outside level-s valid area
-                    if (!col_alloc[i]) break;
-                    // above the buffer: skip this level only; level s+1 sits R planes lower
-                    // (a ghost plane there, so it never reads this level's value)
-                    if (k >= p.Zloc) continue;
-                    const int kg = k + p.zoff;
-                    const bool plane_ghost = kg < R || kg >= R + p.nzg;
-                    const long long gidx = (long long)k * p.plane + colidx[i];
+                    for (int d = 0; d < Q; ++d) pl[d] = ring0 + ((g - 2 * R + d) % NR0) * CELLS;
+                } else {
+#pragma unroll
+                    for (int d = 0; d < Q; ++d)
+                        pl[d] = ringL + ((s - 2) * Q + (k - R + d + KOFF) % Q) * CELLS;
+                }
+                const double* aux = NAUX > 0 ? auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE : nullptr;
+                const double* uprev_pl = nullptr;  // const25pt: level s-2 at plane k
+                if constexpr (KIND == K_CONST25) {
+                    if (s == 2) uprev_pl = ring0 + ((g - 2 * R) % NR0) * CELLS;
+                    else if (s > 2) uprev_pl = ringL + ((s - 3) * Q + (k + KOFF) % Q) * CELLS;
+                }
 
-                    // pointers to the level-(s-1) planes k-R .. k+R (dz index 0..2R)
-                    const double* pl[Q];
-                    if (s == 1) {
+                // (1) stencil for every cell of the valid rows; lanes outside the valid area in
+                //     x compute garbage that no valid cell ever reads (guard rows keep the
+                //     smem reads in bounds)
+                double val[CPT];
 #pragma unroll
-                        for (int d = 0; d < Q; ++d)
-                            pl[d] = ring0 + int((g - 2 * R + d) % NR0) * CELLS;
-                    } else {
-                        const double* base = ringL + (s - 2) * Q * CELLS;
-#pragma unroll
-                        for (int d = 0; d < Q; ++d)
-                            pl[d] = base + ((k - R + d + KOFF) % Q) * CELLS;
-                    }
+                for (int i = 0; i < CPT; ++i) {
+                    val[i] = 0.0;
+                    if (dyv[i] < s * R) continue;  // warp-uniform
                     const int c = lcell[i];
                     auto V = [&](int dx, int dy, int dz) -> double {
-                        if (dz == R && s > 1) return newest;
+                        if (dz == R && s > 1) return newest[i];
                         return pl[dz + R][c + dx + dy * LX];
                     };
-
-                    double val;
-                    if (plane_ghost || col_ghost[i]) {
-                        val = __ldg(&p.ghost[(p.parity0 + s) & 1][gidx]);
-                    } else if constexpr (KIND == K_CONST7) {
+                    auto Cf = [&](int a) -> double { return aux[a * AYX + ai[i]]; };
+                    double v;
+                    if constexpr (KIND == K_CONST7) {
                         const double c0 = p.cc[0], c1 = p.cc[1];
-                        val = dmul(c0, V(0, 0, 0));
-                        val = dadd(val, dmul(c1, dadd(V(1, 0, 0), V(-1, 0, 0))));
-                        val = dadd(val, dmul(c1, dadd(V(0, 1, 0), V(0, -1, 0))));
-                        val = dadd(val, dmul(c1, dadd(V(0, 0, 1), V(0, 0, -1))));
+                        v = dmul(c0, V(0, 0, 0));
+                        v = dadd(v, dmul(c1, dadd(V(1, 0, 0), V(-1, 0, 0))));
+                        v = dadd(v, dmul(c1, dadd(V(0, 1, 0), V(0, -1, 0))));
+                        v = dadd(v, dmul(c1, dadd(V(0, 0, 1), V(0, 0, -1))));
                     } else if constexpr (KIND == K_VAR7) {
-                        val = dmul(__ldg(&p.coeff[0][gidx]), V(0, 0, 0));
-                        val = dadd(val, dmul(__ldg(&p.coeff[1][gidx]), V(1, 0, 0)));
-                        val = dadd(val, dmul(__ldg(&p.coeff[2][gidx]), V(-1, 0, 0)));
-                        val = dadd(val, dmul(__ldg(&p.coeff[3][gidx]), V(0, 1, 0)));
-                        val = dadd(val, dmul(__ldg(&p.coeff[4][gidx]), V(0, -1, 0)));
-                        val = dadd(val, dmul(__ldg(&p.coeff[5][gidx]), V(0, 0, 1)));
-                        val = dadd(val, dmul(__ldg(&p.coeff[6][gidx]), V(0, 0, -1)));
+                        v = dmul(Cf(0), V(0, 0, 0));
+                        v = dadd(v, dmul(Cf(1), V(1, 0, 0)));
+                        v = dadd(v, dmul(Cf(2), V(-1, 0, 0)));
+                        v = dadd(v, dmul(Cf(3), V(0, 1, 0)));
+                        v = dadd(v, dmul(Cf(4), V(0, -1, 0)));
+                        v = dadd(v, dmul(Cf(5), V(0, 0, 1)));
+                        v = dadd(v, dmul(Cf(6), V(0, 0, -1)));
                     } else if constexpr (KIND == K_CONST25) {
                         const double vc = V(0, 0, 0);
                         double lap = dmul(p.cc[0], vc);
@@ -306,45 +428,76 @@ __global__ void __launch_bounds__(NT, 1)
                             sr = dadd(sr, V(0, 0, -r));
                             lap = dadd(lap, dmul(p.cc[r], sr));
                         }
-                        // level s-2 at the centre: t0-1 from src_prev, else the level-(s-2) ring
-                        double uprev;
-                        if (s == 1) {
-                            uprev = p.src_prev[gidx];
-                        } else if (s == 2) {
-                            uprev = ring0[int((g - 2 * R) % NR0) * CELLS + c];
-                        } else {
-                            const double* b2 = ringL + (s - 3) * Q * CELLS;
-                            uprev = b2[((k + KOFF) % Q) * CELLS + c];
-                        }
-                        val = dadd(dsub(dmul(2.0, vc), uprev),
-                                   dmul(__ldg(&p.coeff[0][gidx]), lap));
+                        const double uprev = s == 1 ? Cf(1) : uprev_pl[c];
+                        v = dadd(dsub(dmul(2.0, vc), uprev), dmul(Cf(0), lap));
                     } else {  // K_VAR25
-                        val = dmul(__ldg(&p.coeff[0][gidx]), V(0, 0, 0));
+                        v = dmul(Cf(0), V(0, 0, 0));
 #pragma unroll
                         for (int r = 1; r <= 4; ++r) {
                             const int b = 3 * (r - 1);
-                            val = dadd(val, dmul(__ldg(&p.coeff[b + 1][gidx]),
-                                                 dadd(V(r, 0, 0), V(-r, 0, 0))));
-                            val = dadd(val, dmul(__ldg(&p.coeff[b + 2][gidx]),
-                                                 dadd(V(0, r, 0), V(0, -r, 0))));
-                            val = dadd(val, dmul(__ldg(&p.coeff[b + 3][gidx]),
-                                                 dadd(V(0, 0, r), V(0, 0, -r))));
+                            v = dadd(v, dmul(Cf(b + 1), dadd(V(r, 0, 0), V(-r, 0, 0))));
+                            v = dadd(v, dmul(Cf(b + 2), dadd(V(0, r, 0), V(0, -r, 0))));
+                            v = dadd(v, dmul(Cf(b + 3), dadd(V(0, 0, r), V(0, 0, -r))));
                         }
                     }
-
-                    if (s < TB) {
-                        ringL[((s - 1) * Q + (k + KOFF) % Q) * CELLS + c] = val;
-                        newest = val;
-                    } else {
-                        // level TB: output tile cells of interior planes [za, zb)
-                        if (out_col[i] && !col_ghost[i] && k >= ug.za && k < ug.zb) {
-                            p.dst_final[gidx] = val;
-                            if (p.dst_penult) p.dst_penult[gidx] = V(0, 0, 0);
-                        }
+                    val[i] = v;
+                }
+                // (2) ghost cells of level s hold the parity-(t0+s) field's ghosts (block edges
+                //     and ghost planes only: a uniform branch elsewhere)
+                if (plane_ghost || any_ghost_col) {
+                    const double* ghost = p.ghost[(p.parity0 + s) & 1] + (long long)k * p.plane;
+                    const uint32_t fix = plane_ghost ? ok_mask : col_fix;
+#pragma unroll
+                    for (int i = 0; i < CPT; ++i)
+                        if (dyv[i] >= s * R && ((fix >> i) & 1)) val[i] = __ldg(ghost + colidx[i]);
+                }
+                // (3) results: the level-s ring (s < TB) or the output staging plane (s == TB)
+                if (s < TB) {
+                    double* wr = ringL + ((s - 1) * Q + (k + KOFF) % Q) * CELLS;
+#pragma unroll
+                    for (int i = 0; i < CPT; ++i) {
+                        if (dyv[i] < s * R) continue;
+                        wr[lcell[i]] = val[i];
+                        newest[i] = val[i];
                     }
+                } else if (k >= ug.za && k < ug.zb) {
+                    double* stg = stage + (g & 1) * STAGE;
+#pragma unroll
+                    for (int i = 0; i < CPT; ++i)
+                        if ((out_mask >> i) & 1) stg[sidx[i]] = val[i];  // clipped by omap
+                    if (has_penult) {  // final pass only: level TB-1 of the same cells
+                        double* pen = p.dst_penult + (long long)k * p.plane;
+#pragma unroll
+                        for (int i = 0; i < CPT; ++i)
+                            if ((out_mask >> i) & 1 && !((ghost_mask >> i) & 1))
+                                pen[colidx[i]] = pl[R][lcell[i]];
+                    }
+                    staged = true;
                 }
             }
+            // hand the staged output plane to the async proxy; thread 0 stores it next iteration
+            if (staged) {
+                fence_proxy_async_smem();
+                if (tid == 0) {
+                    pend = true;
+                    pend_x = ug.tx * p.ox;
+                    pend_y = ug.ty * OY;
+                    pend_z = j - H - p.zout_lo;
+                    pend_b = int(g & 1);
+                }
+            }
+            // the store issued at the top of this iteration must finish reading its staging
+            // plane before the next iteration overwrites that plane
+            if (tid == 0) bulk_wait_read_all();
         }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (pend) {
+            tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
+            bulk_commit();
+        }
+        bulk_wait_all();
     }
 }
 

@@ -1,0 +1,42 @@
+"""Per-kind / per-variant throughput sweep (device-resident, CUDA-event timed).
+
+  python tools/sweep.py [--kinds 0,1,2,3] [--n 512] [--nt 20] [--reps 2] [--variants all|default]
+Prints one JSON line per (kind, variant) with MLUP/s, avg pass ms and effective GB/s.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1510_04995_b200 as g  # noqa: E402
+
+B1 = {0: 16, 1: 72, 2: 32, 3: 120}
+ap = argparse.ArgumentParser()
+ap.add_argument("--kinds", default="0,1,2,3")
+ap.add_argument("--n", type=int, default=512)
+ap.add_argument("--nt", type=int, default=24)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--variants", default="all")
+ap.add_argument("--zchunks", type=int, default=0)
+a = ap.parse_args()
+for kind in [int(k) for k in a.kinds.split(",")]:
+    vs = [v for v in g.variants() if v["kind"] == kind]
+    grid = g.GridSpec(a.n, a.n, a.n, 0)
+    with g.DeviceState.seeded(kind, grid, 42, remap=True) as ds:
+        for v in vs:
+            ds.set_config(g.GpuConfig(tb=v["tb"], variant=v["index"], zchunks=a.zchunks))
+            ds.step(a.nt)
+            best = None
+            for _ in range(a.reps):
+                r = ds.step(a.nt)
+                if best is None or r.kernel_seconds < best.kernel_seconds:
+                    best = r
+            avg = best.pass_seconds / best.n_launches
+            print(json.dumps({"kind": g.KINDS[kind], "n": a.n, "tb": v["tb"], "variant": v["index"],
+                              "lx": v["lx"], "ly": v["ly"], "mlups": round(best.mlups),
+                              "avg_pass_ms": round(avg * 1e3, 4), "passes": best.n_launches,
+                              "eff_GBs": round(a.n ** 3 * B1[kind] / avg / 1e9, 1),
+                              "zchunks": best.zchunks_used, "grid": best.grid_ctas,
+                              "redundancy": round(best.computed_lups / best.lups, 3)}), flush=True)
