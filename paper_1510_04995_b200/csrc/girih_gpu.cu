@@ -358,6 +358,7 @@ struct Slab {
     int zout_lo = 0, zout_hi = 0;  // own interior planes (local)
     std::unique_ptr<DevBuf> buf[4];     // u, v, scratch even, scratch odd
     std::unique_ptr<DevBuf> cblock;     // coefficient fields, contiguous [c][k][j][i]
+    std::unique_ptr<DevBuf> work;       // dynamic work counters of the zwave launches
     double* coeff(int c, size_t slab_elems) const { return cblock->p + size_t(c) * slab_elems; }
     cudaEvent_t done = nullptr;    // end of this slab's work in the current pass
 };
@@ -474,6 +475,7 @@ void setup_slabs(Handle& h) {
         alloc_buf(s.buf[0], s.device, n, s.stream);
         alloc_buf(s.buf[1], s.device, n, s.stream);
         if (h.nc > 0) alloc_buf(s.cblock, s.device, n * h.nc, s.stream);
+        alloc_buf(s.work, s.device, 32, s.stream);
     }
     if (!h.emulated && nslab > 1) {
         for (int g = 0; g + 1 < nslab; ++g) {
@@ -636,22 +638,15 @@ const CUtensorMap& tensor_map(Handle& h, int slab, const double* base, int narr,
     return h.maps.back()->map;
 }
 
-// z chunks per tile column: minimise (waves of units) x (planes streamed per unit)
-int choose_zchunks(int tiles_xy, int nzl, int grid, int H) {
-    int best = 1;
-    double best_cost = 1e300;
-    const int max_chunks = std::max(1, nzl / std::max(8, 2 * H));
-    for (int c = 1; c <= max_chunks; ++c) {
-        const int len = (nzl + c - 1) / c;
-        const long long units = (long long)tiles_xy * c;
-        const long long waves = (units + grid - 1) / grid;
-        const double cost = double(waves) * double(len + 2 * H);
-        if (cost < best_cost * 0.999) {
-            best_cost = cost;
-            best = c;
-        }
-    }
-    return best;
+// z chunks per tile column. Units are drawn dynamically in z-chunk-major order, so short chunks
+// keep every tile in flight within ~one chunk of its neighbours (halo rows stay in L2) and
+// balance the load; each chunk re-streams 2H extra level-0 planes (L2 hits) and recomputes
+// 2(TB-s)R planes of level s, so chunks grow with the fused depth.
+int choose_zchunks(int nzl, int H, int ncoeff) {
+    // coefficient-heavy kinds: each chunk boundary re-streams (TB-1)R coefficient planes that
+    // no longer sit in L2 (16.8 MB per 512^2 plane for var7pt), so their chunks are longer
+    const int len = ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
+    return std::max(1, (nzl + len - 1) / len);
 }
 
 struct LaunchInfo {
@@ -698,11 +693,11 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
     const int max_grid = h.sm_count * occ;
     const int txy = p.tiles_x * p.tiles_y;
-    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
-                              : choose_zchunks(txy, nzl, max_grid, H);
+    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl) : choose_zchunks(nzl, H, h.nc);
     p.zc_len = (nzl + p.nzc - 1) / p.nzc;
     p.nzc = (nzl + p.zc_len - 1) / p.zc_len;
     p.units = txy * p.nzc;
+    p.work = reinterpret_cast<int*>(s.work->p);
     li->grid = std::min(p.units, max_grid);
     li->zchunks = p.nzc;
     // computed LUPs: level s covers (OX + 2(TB-s)R) x (OY + 2(TB-s)R) per tile column and
@@ -796,6 +791,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 umap = &tensor_map(h, int(g), s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
             const CUtensorMap& omap = tensor_map(h, int(g), s.buf[ps.dst]->p, 1, p.ox,
                                                  var->ly - 2 * ps.tb * h.R, 1);
+            GCHECK(cudaMemsetAsync(p.work, 0, sizeof(int), s.stream));
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi], s.stream));
             GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi + 1], s.stream));

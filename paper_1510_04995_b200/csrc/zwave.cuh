@@ -67,6 +67,7 @@ struct PassParams {
     int nzc, zc_len;         // z chunks per tile column and output planes per chunk
     int zout_lo, zout_hi;    // local output planes [lo, hi)
     int units;               // tiles_x * tiles_y * nzc
+    int* work;               // dynamic unit counter (zeroed before every launch)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
                              // innermost box coordinate 16-byte aligned (even for fp64)
 };
@@ -86,6 +87,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
@@ -161,32 +166,47 @@ __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
     return g;
 }
 
-// Producer cursor over the CTA's persistent unit list (static round robin over units).
+// Work distribution. Units are ordered z-chunk-major (all tiles of chunk 0, then chunk 1, ...)
+// and handed out dynamically: CTA b starts with unit b, then takes gridDim.x + atomicAdd(work).
+// All tiles in flight therefore sit within about one chunk of each other in z, so the halo rows
+// a tile shares with its neighbours are still in L2 when the neighbour reads them (a static
+// round robin lets CTAs on more crowded SMs drift ~100 planes behind, and every halo row then
+// comes from DRAM a second time). The V producer (thread 0) is the only thread that draws units;
+// it publishes them in a small smem queue that the aux producer and the consumers replay.
+constexpr int UQ = 8;  // unit queue depth (the producer runs at most a few units ahead)
+
 struct Cursor {
-    int u, it, n_it;
+    int seq;   // this CTA's unit sequence number
+    int u;     // unit id (>= units: exhausted)
+    int it, n_it;
     UnitGeom ug;
 };
 
 template <int H>
-__device__ __forceinline__ void cursor_init(Cursor& c, const PassParams& p) {
-    c.u = blockIdx.x;
+__device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int seq, int u) {
+    c.seq = seq;
+    c.u = u;
     c.it = 0;
     c.n_it = 0;
-    if (c.u < p.units) {
-        c.ug = unit_geom(p, c.u);
+    if (u < p.units) {
+        c.ug = unit_geom(p, u);
         c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
     }
 }
 
-template <int H>
-__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p) {
+// advance within / across units; the drawing cursor (V producer) fetches new unit ids
+template <int H, bool DRAW>
+__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, volatile int* uq) {
     if (++c.it >= c.n_it) {
-        c.it = 0;
-        c.u += gridDim.x;
-        if (c.u < p.units) {
-            c.ug = unit_geom(p, c.u);
-            c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
+        int next;
+        if (DRAW) {
+            next = gridDim.x + atomicAdd(p.work, 1);
+            if (next > p.units) next = p.units;
+            uq[(c.seq + 1) % UQ] = next;
+        } else {
+            next = uq[(c.seq + 1) % UQ];
         }
+        cursor_set<H>(c, p, c.seq + 1, next);
     }
 }
 
@@ -265,6 +285,7 @@ __global__ void __launch_bounds__(NT, MINB)
     __syncthreads();
 
     // ---- producers (thread 0): V runs P elements ahead, aux PA elements ahead ----
+    __shared__ int uq[UQ];
     Cursor vcur{}, acur{};
     uint32_t vnext = G0, anext = G0;
     auto issue_v = [&]() {
@@ -276,7 +297,7 @@ __global__ void __launch_bounds__(NT, MINB)
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
         tma_load_plane(ring0 + slot * CELLS, &vmap, xd, yd, j, &vbar[slot]);
         ++vnext;
-        cursor_next<H>(vcur, p);
+        cursor_next<H, true>(vcur, p, uq);
     };
     auto issue_a = [&]() {
         if constexpr (NAUX > 0) {
@@ -285,6 +306,14 @@ __global__ void __launch_bounds__(NT, MINB)
             const int slot = int(anext % NAR);
             const int xd = p.off + acur.ug.tx * p.ox + R - p.hx + AXO;
             const int yd = acur.ug.ty * OY + R - H + AYO;
+            if (acur.it < 2 * R) {
+                // no level reads the aux plane of the first 2R iterations of a unit: complete
+                // the phase without moving data
+                mbar_arrive(&abar[slot]);
+                ++anext;
+                cursor_next<H, false>(acur, p, uq);
+                return;
+            }
             mbar_arrive_expect_tx(&abar[slot], AUX_BYTES);
             double* dst = auxr + slot * AUXPLANE;
             if constexpr (KIND == K_CONST25) {
@@ -294,12 +323,15 @@ __global__ void __launch_bounds__(NT, MINB)
                 tma_load_4d(dst, &cmap, xd, yd, k1, 0, &abar[slot]);
             }
             ++anext;
-            cursor_next<H>(acur, p);
+            cursor_next<H, false>(acur, p, uq);
         }
     };
+    static_assert(P >= PA, "the V producer draws units and must lead the aux producer");
     if (tid == 0) {
-        cursor_init<H>(vcur, p);
-        cursor_init<H>(acur, p);
+        const int u0 = blockIdx.x < p.units ? int(blockIdx.x) : p.units;
+        uq[0] = u0;
+        cursor_set<H>(vcur, p, 0, u0);
+        cursor_set<H>(acur, p, 0, u0);
         for (int e = 0; e < P; ++e) issue_v();
         for (int e = 0; e < PA; ++e) issue_a();
     }
@@ -323,8 +355,11 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     const bool has_penult = p.dst_penult != nullptr;
 
+    __syncthreads();  // uq[0] visible
     uint32_t g = G0;  // consumer's global element index
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int seq = 0;; ++seq) {
+        const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
+        if (u >= p.units) break;
         const UnitGeom ug = unit_geom(p, u);
         const int n_it = (ug.zb - ug.za) + 2 * H;
         const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
