@@ -141,6 +141,10 @@ int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_pass
                    int* n_passes, int* pass_tb, int* pass_src, int* pass_src_prev,
                    int* pass_dst, int* pass_dst_penult);
 
+/* z-slab decomposition used by multi-GPU handles: slab g of nslabs owns interior planes
+ * [*z0, *z1) (0-based interior z) and carries *hz halo planes per side (R * max fused depth). */
+int girih_gpu_slab_layout(int kind, int nz, int nslabs, int g, int* z0, int* z1, int* hz);
+
 /* On-device auto-tuner (replaces girih::tune, proj/src/tuner.cpp:146-210): hill-climbs
  * (tb, variant, zchunks) with CUDA-event timing and adaptive test sizing on the handle's
  * own state (the state is restored afterwards). Writes the best config into *best. */

@@ -83,6 +83,7 @@ SIGNATURES = {
                                 C.POINTER(GirihGpuConfig), C.POINTER(GirihGpuReport)]),
     "girih_gpu_plan": (C.c_int, [C.c_int, C.c_longlong, C.c_longlong, C.c_int, C.c_int,
                                  _ip, _ip, _ip, _ip, _ip, _ip]),
+    "girih_gpu_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ip]),
     "girih_gpu_tune": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(GirihGpuConfig), _dp, _ip]),
     "girih_gpu_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "girih_gpu_host_free": (C.c_int, [C.c_void_p]),

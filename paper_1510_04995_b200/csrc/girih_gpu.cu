@@ -433,6 +433,12 @@ void validate_config(const girih_gpu_config& c, int kind) {
 // Slab layout. ngpus > 1 spreads slabs over devices [device, device + ngpus); the
 // GIRIH_EMULATE_SLABS reserved flag (cfg.reserved > 0) places cfg.reserved slabs on ONE device
 // (used by the single-GPU tests of the decomposition).
+// slab g of n: interior planes [z0, z1) and halo depth (R * max compiled fused depth)
+void slab_bounds(int nz, int n, int g, int* z0, int* z1) {
+    *z0 = int((long long)nz * g / n);
+    *z1 = int((long long)nz * (g + 1) / n);
+}
+
 void setup_slabs(Handle& h) {
     int nslab = h.cfg.ngpus;
     h.emulated = false;
@@ -451,7 +457,8 @@ void setup_slabs(Handle& h) {
     for (int g = 0; g < nslab; ++g) {
         Slab& s = h.slabs[g];
         s.device = h.emulated ? h.cfg.device : h.cfg.device + g;
-        const int z0 = int((long long)h.nz * g / nslab), z1 = int((long long)h.nz * (g + 1) / nslab);
+        int z0, z1;
+        slab_bounds(h.nz, nslab, g, &z0, &z1);
         if (nslab == 1) {
             s.Zloc = h.Z;
             s.zoff = 0;
@@ -1238,6 +1245,19 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         best->zchunks = zopts[bz];
         if (best_mlups) *best_mlups = bs;
         if (n_measured) *n_measured = measured;
+    });
+}
+
+int girih_gpu_slab_layout(int kind, int nz, int nslabs, int g, int* z0, int* z1, int* hz) {
+    return guarded([&] {
+        const KindInfo& k = kind_info(kind);
+        if (nslabs < 1 || g < 0 || g >= nslabs || nz < nslabs)
+            throw_err(GIRIH_EINVAL, "bad slab decomposition");
+        int a, b;
+        slab_bounds(nz, nslabs, g, &a, &b);
+        if (z0) *z0 = a;
+        if (z1) *z1 = b;
+        if (hz) *hz = nslabs == 1 ? k.radius : k.radius * max_tb(kind);
     });
 }
 

@@ -214,6 +214,14 @@ def plan(kind: int, t0: int, steps: int, tb: int):
     return [tuple(a[i] for a in arrs) for i in range(n.value)]
 
 
+def slab_layout(kind: int, nz: int, nslabs: int, g: int):
+    """(z0, z1, hz): interior planes [z0, z1) of slab g and its halo depth (multi-GPU z-slabs)."""
+    z0, z1, hz = C.c_int(), C.c_int(), C.c_int()
+    check(load().girih_gpu_slab_layout(int(kind), int(nz), int(nslabs), int(g), C.byref(z0),
+                                       C.byref(z1), C.byref(hz)))
+    return z0.value, z1.value, hz.value
+
+
 def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     """A numpy array in page-locked host memory (freed when the array is collected)."""
     nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
