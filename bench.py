@@ -174,7 +174,8 @@ def run_reference_arm(args, rank: int):
     lups = n ** 3 * steps_per * args.steps
     value = lups / dt / 1e6
     line = {
-        "impl": "reference", "metric": f"fp64 MLUP/s ({KINDS[kind]} {n}^3)", "value": value,
+        "impl": "reference", "metric": f"fp64 MLUP/s ({KINDS[kind]} {n}^3, {args.nt} steps)",
+        "value": value,
         "unit": "MLUP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded init_state + remap)",
@@ -200,11 +201,25 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     T = args.nt
     dev = local_rank
     hbm, hbm_src = measured_peaks()
-    grid = g.GridSpec(n, n, n, 0)
     cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant)
+    dist = None
     if world > 1:
-        raise SystemExit("multi-rank bench path: see run_gpu_multirank")
-    ds = g.DeviceState.seeded(kind, grid, 42, remap=True, config=cfg)
+        # weak scaling: a 512 x 512 x (512 N) grid in z-slabs, one slab per rank/GPU, R*TB halos
+        # exchanged over NCCL after every pass (inside the library); torch.distributed is the
+        # plumbing for the NCCL id and the max-over-ranks timing
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(g.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+        ds = g.DeviceState.slab_seeded(kind, g.GridSpec(n, n, n * world), 42, True, rank, world,
+                                       nid, cfg)
+    else:
+        ds = g.DeviceState.seeded(kind, g.GridSpec(n, n, n), 42, remap=True, config=cfg)
     tuned = None
     if args.tune:
         tcfg, tml, nmeas = ds.tune(max_tb=args.tb if args.tb > 0 else 0)
@@ -214,25 +229,38 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                  "mlups": tml, "measured": nmeas}
     for _ in range(args.warmup):
         ds.step(T)
+    if dist is not None:
+        import torch
+        dist.barrier()
+        torch.cuda.synchronize()
     reps = []
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             reps.append(ds.step(T))
+    if dist is not None:
+        dist.barrier()
+        torch.cuda.synchronize()
     kernel_s = sum(r.kernel_seconds for r in reps)
-    lups = sum(r.lups for r in reps)
+    if dist is not None:  # device time, max over ranks
+        tk = torch.tensor([kernel_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+        kernel_s = float(tk.item())
+    cells = n ** 3  # per GPU
+    lups = cells * world * T * args.steps
     value = lups / kernel_s / 1e6
     launches = sum(r.n_launches for r in reps)
     pass_s = sum(r.pass_seconds for r in reps)
     avg_launch = pass_s / max(1, launches)
-    cells = n ** 3
     achieved = cells * B1[kind] / avg_launch / 1e9  # algorithmic bytes per launch / duration
     traffic, traffic_src = ncu_traffic(kind, n)
     r0 = reps[-1]
     ds.close()
 
     # ---- e2e: the drop-in C-ABI call on pinned host buffers (H2D + sweep + D2H timed) ----
+    # (N > 1: every rank runs the drop-in call on its own 512^3 host state; max over ranks)
     e2e = None
     if not args.no_e2e:
+        grid = g.GridSpec(n, n, n, 0)
         with g.DeviceState.seeded(kind, grid, 42, remap=True, config=cfg) as ds2:
             host = ds2.download(pinned=True)
         e2e_cfg = g.GpuConfig(tb=r0.tb_used, variant=r0.variant_used, zchunks=args.zchunks,
@@ -244,12 +272,17 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
             if rep > 0:  # first call is the warm-up
                 walls.append(pr.wall_seconds)
                 h2d, d2h = pr.h2d_bytes, pr.d2h_bytes
-        e2e = {"value": cells * T / (sum(walls) / len(walls)) / 1e6, "unit": "MLUP/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": sum(walls) / len(walls) * 1e3}
+        wall = sum(walls) / len(walls)
+        if dist is not None:
+            tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+            wall = float(tw.item())
+        e2e = {"value": cells * world * T / wall / 1e6, "unit": "MLUP/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": wall * 1e3}
 
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1 and rank == 0:
         cpu = cpu_reference_sample(kind, n, args.cpu_target_s, 100)
         cpu.pop("walls", None)
         cpu.pop("steps", None)
@@ -275,7 +308,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                    "tb": r0.tb_used, "variant": r0.variant_used, "zchunks": r0.zchunks_used,
                    "grid_ctas": r0.grid_ctas, "passes_per_step": r0.n_launches,
                    "l2": f"inputs {cells * 8 * (2 + (7 if kind == 1 else 13 if kind == 3 else kind // 2)) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                   "global_grid": [n, n, n * world],
+                   "parallelism": (f"z-slabs x{world} (NCCL halo exchange of R*TB planes per pass)"
+                                   if world > 1 else "single GPU"),
                    "tuned": tuned},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -293,6 +328,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
     return 0
 
 

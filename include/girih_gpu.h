@@ -114,6 +114,16 @@ int girih_gpu_open(const girih_state_view* state, const girih_gpu_config* cfg, v
 int girih_gpu_open_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned long long seed,
                           int remap, const girih_gpu_config* cfg, void** handle);
 
+/* Multi-process z-slabs (one process per GPU): rank 0 creates an NCCL unique id (len >= 128
+ * bytes) and shares it; every rank then opens its own slab of the global nx x ny x nz grid on
+ * cfg->device, initialised on the device from the global counter-based generator. step()
+ * exchanges R*TB halos with ranks rank-1 / rank+1 over NCCL after every pass; download()
+ * fills this slab's planes (plus the global ghost planes at the outer slabs) of a global view. */
+int girih_gpu_nccl_unique_id(unsigned char* id, int len);
+int girih_gpu_open_slab_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned long long seed,
+                               int remap, int rank, int nranks, const unsigned char* nccl_id,
+                               const girih_gpu_config* cfg, void** handle);
+
 /* Re-upload u, v, coefficients, cc and t_current from a host view of the same shape. */
 int girih_gpu_upload(void* handle, const girih_state_view* state);
 

@@ -6,13 +6,14 @@ is its host-side mirror of the reference's stencil/run interface.
 from ._lib import GirihError, InvalidArgument, LIB_PATH, load
 from .stencil import (CONST7PT, CONST25PT, KINDS, VAR7PT, VAR25PT, DeviceState, GpuConfig,
                       GridSpec, PerfReport, ProblemState, StencilTraits, device_info, fp64_peak,
-                      init_state, interior_checksum, pinned_empty, plan, run, slab_layout,
+                      init_state, interior_checksum, nccl_unique_id, pinned_empty, plan, run,
+                      slab_layout,
                       stencil_from_name,
                       traits, variants)
 
 __all__ = [
     "CONST7PT", "VAR7PT", "CONST25PT", "VAR25PT", "KINDS", "DeviceState", "GpuConfig", "GridSpec",
     "PerfReport", "ProblemState", "StencilTraits", "GirihError", "InvalidArgument", "LIB_PATH",
-    "device_info", "fp64_peak", "init_state", "interior_checksum", "load", "pinned_empty", "plan",
+    "device_info", "fp64_peak", "init_state", "interior_checksum", "load", "nccl_unique_id", "pinned_empty", "plan",
     "run", "slab_layout", "stencil_from_name", "traits", "variants",
 ]

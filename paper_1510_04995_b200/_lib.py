@@ -72,6 +72,10 @@ SIGNATURES = {
     "girih_gpu_open_seeded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         C.c_ulonglong, C.c_int, C.POINTER(GirihGpuConfig),
                                         C.POINTER(C.c_void_p)]),
+    "girih_gpu_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "girih_gpu_open_slab_seeded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_ulonglong, C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                             C.POINTER(GirihGpuConfig), C.POINTER(C.c_void_p)]),
     "girih_gpu_upload": (C.c_int, [C.c_void_p, C.POINTER(GirihStateView)]),
     "girih_gpu_step": (C.c_int, [C.c_void_p, C.c_longlong, C.POINTER(GirihGpuReport)]),
     "girih_gpu_download": (C.c_int, [C.c_void_p, C.POINTER(GirihStateView)]),

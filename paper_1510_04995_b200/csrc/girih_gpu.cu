@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -351,6 +353,7 @@ struct DevBuf {
 
 // One z-slab: local planes [0, Zloc) hold global allocated planes [zoff, zoff + Zloc).
 struct Slab {
+    int gidx = 0, gcount = 1;  // position of this slab in the global decomposition
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -374,6 +377,9 @@ struct Handle {
     int hz = 0;  // halo planes per slab side
     std::vector<Slab> slabs;
     bool emulated = false;  // several slabs on one device
+    // multi-process mode: this process owns slab `rank` of `nranks`; halos move over NCCL
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
     int sm_count = 0;
     // timing events (slab 0 stream)
     std::vector<cudaEvent_t> ev;
@@ -388,6 +394,50 @@ struct Handle {
     size_t plane_elems() const { return size_t(pitch) * Y; }
     size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
 };
+
+// NCCL is resolved at run time (dlopen) so single-GPU users need no NCCL; in a process that
+// already loaded NCCL (e.g. torch's), RTLD_NOLOAD picks up that copy.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (loaded) return api;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) throw_err(GIRIH_ENCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+        void* f = dlsym(lib, n);
+        if (!f) throw_err(GIRIH_ENCCL, std::string("NCCL symbol missing: ") + n);
+        return f;
+    };
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+    api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+    return api;
+}
+
+#define NCHECK(expr)                                                                    \
+    do {                                                                                \
+        ncclResult_t r_ = (expr);                                                       \
+        if (r_ != ncclSuccess)                                                          \
+            throw_err(GIRIH_ENCCL, std::string(#expr) + ": " + nccl().errorString(r_)); \
+    } while (0)
 
 void alloc_buf(std::unique_ptr<DevBuf>& b, int device, size_t elems, cudaStream_t st) {
     if (b) return;
@@ -446,20 +496,25 @@ void setup_slabs(Handle& h) {
         nslab = h.cfg.reserved;
         h.emulated = true;
     }
-    if (nslab > h.nz) throw_err(GIRIH_EINVAL, "more z-slabs than interior planes");
+    const bool dist = h.nranks > 1;
+    const int gcount = dist ? h.nranks : nslab;
+    if (dist) nslab = 1;
+    if (gcount > h.nz) throw_err(GIRIH_EINVAL, "more z-slabs than interior planes");
     int ndev = 0;
     GCHECK(cudaGetDeviceCount(&ndev));
-    if (!h.emulated && h.cfg.device + nslab > ndev)
+    if (!h.emulated && !dist && h.cfg.device + nslab > ndev)
         throw_err(GIRIH_EINVAL, "not enough CUDA devices for ngpus");
     if (h.cfg.device < 0 || h.cfg.device >= ndev) throw_err(GIRIH_EINVAL, "bad CUDA device");
-    h.hz = (nslab == 1) ? h.R : h.R * max_tb(h.kind);
+    h.hz = (gcount == 1) ? h.R : h.R * max_tb(h.kind);
     h.slabs.resize(nslab);
     for (int g = 0; g < nslab; ++g) {
         Slab& s = h.slabs[g];
-        s.device = h.emulated ? h.cfg.device : h.cfg.device + g;
+        s.gidx = dist ? h.rank : g;
+        s.gcount = gcount;
+        s.device = (h.emulated || dist) ? h.cfg.device : h.cfg.device + g;
         int z0, z1;
-        slab_bounds(h.nz, nslab, g, &z0, &z1);
-        if (nslab == 1) {
+        slab_bounds(h.nz, gcount, s.gidx, &z0, &z1);
+        if (gcount == 1) {
             s.Zloc = h.Z;
             s.zoff = 0;
             s.zout_lo = h.R;
@@ -535,14 +590,14 @@ void copy_d2h(Handle& h, double* const dev_of_slab[], double* host) {
     for (size_t g = 0; g < h.slabs.size(); ++g) {
         Slab& s = h.slabs[g];
         int k0, k1;  // global planes this slab is authoritative for
-        if (h.slabs.size() == 1) {
+        if (s.gcount == 1) {
             k0 = 0;
             k1 = h.Z;
         } else {
             k0 = s.zout_lo + s.zoff;
             k1 = s.zout_hi + s.zoff;
-            if (g == 0) k0 = 0;                          // lower ghost planes
-            if (g + 1 == h.slabs.size()) k1 = h.Z;       // upper ghost planes
+            if (s.gidx == 0) k0 = 0;                     // lower ghost planes
+            if (s.gidx + 1 == s.gcount) k1 = h.Z;        // upper ghost planes
         }
         GCHECK(cudaSetDevice(s.device));
         double* dst = host + (size_t)k0 * h.Y * h.X;
@@ -732,10 +787,30 @@ struct StepStats {
 };
 
 void exchange_halos(Handle& h, int buf) {
-    const int ns = int(h.slabs.size());
-    if (ns < 2) return;
     const size_t pe = h.plane_elems();
     const int hz = h.hz;
+    if (h.nranks > 1) {  // multi-process: one slab per rank, neighbours rank-1 / rank+1 over NCCL
+        Slab& s = h.slabs[0];
+        GCHECK(cudaSetDevice(s.device));
+        double* b = s.buf[buf]->p;
+        const size_t cnt = (size_t)hz * pe;
+        NcclApi& api = nccl();
+        NCHECK(api.groupStart());
+        if (h.rank > 0) {
+            NCHECK(api.send(b + (size_t)s.zout_lo * pe, cnt, ncclDouble, h.rank - 1, h.comm, s.stream));
+            NCHECK(api.recv(b, cnt, ncclDouble, h.rank - 1, h.comm, s.stream));
+        }
+        if (h.rank + 1 < h.nranks) {
+            NCHECK(api.send(b + (size_t)(s.zout_hi - hz) * pe, cnt, ncclDouble, h.rank + 1, h.comm,
+                            s.stream));
+            NCHECK(api.recv(b + (size_t)s.zout_hi * pe, cnt, ncclDouble, h.rank + 1, h.comm,
+                            s.stream));
+        }
+        NCHECK(api.groupEnd());
+        return;
+    }
+    const int ns = int(h.slabs.size());
+    if (ns < 2) return;
     for (int g = 0; g < ns; ++g) GCHECK(cudaEventRecord(h.slabs[g].done, h.slabs[g].stream));
     for (int g = 0; g < ns; ++g) {
         Slab& s = h.slabs[g];
@@ -808,7 +883,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             st.n_launches++;
         }
         // halo exchange of the levels the next pass reads
-        if (h.slabs.size() > 1) {
+        if (h.slabs.size() > 1 || h.nranks > 1) {
             exchange_halos(h, ps.dst);
             if (h.kind == K_CONST25 && ps.dst_penult >= 0) exchange_halos(h, ps.dst_penult);
         }
@@ -846,6 +921,10 @@ girih_gpu_config default_config() {
 }
 
 void destroy(Handle* h) {
+    if (h->comm) {
+        nccl().commDestroy(h->comm);
+        h->comm = nullptr;
+    }
     for (Slab& s : h->slabs) {
         cudaSetDevice(s.device);
         if (s.stream) cudaStreamSynchronize(s.stream);
@@ -993,6 +1072,44 @@ int girih_gpu_open_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned 
         setup_geometry(*h, kind, nx, ny, nz, pad_x);
         validate_config(h->cfg, h->kind);
         setup_slabs(*h);
+        init_state_device(*h, seed, remap);
+        *handle = h;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_nccl_unique_id(unsigned char* id, int len) {
+    return guarded([&] {
+        if (!id || len < int(sizeof(ncclUniqueId))) throw_err(GIRIH_EINVAL, "id buffer too small");
+        ncclUniqueId u;
+        NCHECK(nccl().getUniqueId(&u));
+        std::memcpy(id, &u, sizeof u);
+    });
+}
+
+int girih_gpu_open_slab_seeded(int kind, int nx, int ny, int nz, int pad_x, unsigned long long seed,
+                               int remap, int rank, int nranks, const unsigned char* nccl_id,
+                               const girih_gpu_config* cfg, void** handle) {
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!handle || !nccl_id) throw_err(GIRIH_EINVAL, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw_err(GIRIH_EINVAL, "bad rank");
+        h = new Handle();
+        h->cfg = cfg ? *cfg : default_config();
+        h->cfg.ngpus = 1;
+        h->cfg.reserved = 0;
+        h->rank = rank;
+        h->nranks = nranks;
+        setup_geometry(*h, kind, nx, ny, nz, pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        if (nranks > 1) {
+            GCHECK(cudaSetDevice(h->slabs[0].device));
+            ncclUniqueId u;
+            std::memcpy(&u, nccl_id, sizeof u);
+            NCHECK(nccl().commInitRank(&h->comm, nranks, u, rank));
+        }
         init_state_device(*h, seed, remap);
         *handle = h;
     });

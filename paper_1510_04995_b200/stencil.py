@@ -214,6 +214,13 @@ def plan(kind: int, t0: int, steps: int, tb: int):
     return [tuple(a[i] for a in arrs) for i in range(n.value)]
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for girih_gpu_open_slab_seeded (call on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    check(load().girih_gpu_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
 def slab_layout(kind: int, nz: int, nslabs: int, g: int):
     """(z0, z1, hz): interior planes [z0, z1) of slab g and its halo depth (multi-GPU z-slabs)."""
     z0, z1, hz = C.c_int(), C.c_int(), C.c_int()
@@ -261,6 +268,20 @@ class DeviceState:
         h = C.c_void_p()
         check(load().girih_gpu_open_seeded(int(kind), grid.nx, grid.ny, grid.nz, grid.pad_x,
                                            int(seed), int(bool(remap)), C.byref(cfg), C.byref(h)))
+        return cls(h, kind, grid, config)
+
+    @classmethod
+    def slab_seeded(cls, kind: int, grid: GridSpec, seed: int, remap: bool, rank: int, nranks: int,
+                    nccl_id: bytes, config: Optional[GpuConfig] = None) -> "DeviceState":
+        """This process's z-slab `rank` of `nranks` of the global grid (one process per GPU);
+        halos move over NCCL. `nccl_id` comes from nccl_unique_id() on rank 0."""
+        config = config or GpuConfig()
+        cfg = config.to_c()
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(bytes(nccl_id), max(len(nccl_id), 128))
+        check(load().girih_gpu_open_slab_seeded(int(kind), grid.nx, grid.ny, grid.nz, grid.pad_x,
+                                                int(seed), int(bool(remap)), int(rank), int(nranks),
+                                                idbuf, C.byref(cfg), C.byref(h)))
         return cls(h, kind, grid, config)
 
     def _handle(self):
