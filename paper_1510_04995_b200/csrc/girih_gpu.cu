@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -314,6 +315,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
+// L2 sector promotion of TMA fills (GIRIH_L2_PROMOTION = 0 / 64 / 128 / 256 overrides)
+CUtensorMapL2promotion l2_promotion() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("GIRIH_L2_PROMOTION");
+        v = e ? std::atoi(e) : 0;
+    }
+    switch (v) {
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    }
+}
+
 // fp64 tiled map: 3-D (x, y, z) over dims {dx, dy, dz}, or 4-D (x, y, z, array) when narr > 1;
 // row pitch / plane / array strides in elements; box bx x by x 1 (x narr)
 CUtensorMap make_map(const double* base, long long dx, long long dy, long long dz, int narr,
@@ -327,8 +343,7 @@ CUtensorMap make_map(const double* base, long long dx, long long dy, long long d
     CUresult r = get_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
                                  const_cast<double*>(base), dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
@@ -362,6 +377,7 @@ struct Slab {
     std::unique_ptr<DevBuf> buf[4];     // u, v, scratch even, scratch odd
     std::unique_ptr<DevBuf> cblock;     // coefficient fields, contiguous [c][k][j][i]
     std::unique_ptr<DevBuf> work;       // dynamic work counters of the zwave launches
+    std::unique_ptr<DevBuf> trace;      // GIRIH_TRACE: per-iteration phase clocks (debug)
     double* coeff(int c, size_t slab_elems) const { return cblock->p + size_t(c) * slab_elems; }
     cudaEvent_t done = nullptr;    // end of this slab's work in the current pass
 };
@@ -760,6 +776,12 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.nzc = (nzl + p.zc_len - 1) / p.zc_len;
     p.units = txy * p.nzc;
     p.work = reinterpret_cast<int*>(s.work->p);
+    p.trace = nullptr;
+    if (std::getenv("GIRIH_TRACE")) {
+        alloc_buf(s.trace, s.device, 4096 * 8, s.stream);
+        GCHECK(cudaMemsetAsync(s.trace->p, 0, 4096 * 8 * 8, s.stream));
+        p.trace = reinterpret_cast<unsigned long long*>(s.trace->p);
+    }
     li->grid = std::min(p.units, max_grid);
     li->zchunks = p.nzc;
     // computed LUPs: level s covers (OX + 2(TB-s)R) x (OY + 2(TB-s)R) per tile column and
@@ -877,6 +899,19 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi], s.stream));
             GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
             if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi + 1], s.stream));
+            if (p.trace) {  // debug: dump CTA 0's phase clocks of this pass
+                std::vector<unsigned long long> tv(4096 * 8);
+                GCHECK(cudaMemcpyAsync(tv.data(), p.trace, tv.size() * 8, cudaMemcpyDeviceToHost,
+                                       s.stream));
+                GCHECK(cudaStreamSynchronize(s.stream));
+                if (FILE* f = std::fopen(std::getenv("GIRIH_TRACE"), "a")) {
+                    for (size_t q = 0; q + 8 <= tv.size(); q += 8)
+                        if (tv[q]) std::fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu %llu\n", pi,
+                                                tv[q], tv[q + 1], tv[q + 2], tv[q + 3], tv[q + 4],
+                                                tv[q + 5], tv[q + 6], tv[q + 7]);
+                    std::fclose(f);
+                }
+            }
             st.computed += li.computed_lups;
             st.grid = li.grid;
             st.zchunks = li.zchunks;

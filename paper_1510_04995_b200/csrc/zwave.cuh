@@ -68,6 +68,7 @@ struct PassParams {
     int zout_lo, zout_hi;    // local output planes [lo, hi)
     int units;               // tiles_x * tiles_y * nzc
     int* work;               // dynamic unit counter (zeroed before every launch)
+    unsigned long long* trace;  // optional per-iteration phase clocks of CTA 0 (debug)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
                              // innermost box coordinate 16-byte aligned (even for fp64)
 };
@@ -224,7 +225,8 @@ struct ZwaveConfig {
     static constexpr int OY = LY - 2 * H;   // output tile height (x: runtime, halo H or H+1)
     static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
-    static constexpr int CPT = CELLS / NT;  // cells per thread
+    static constexpr int PPT = CELLS / (2 * NT);  // x-pairs of cells per thread
+    static constexpr int XA = 2 * ((R + 1) / 2);  // pair-aligned x reach (R=1: 2, R=4: 4)
     static constexpr int NRING = NR0 + (TB - 1) * Q;
     // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
     static constexpr int NAUX = AuxArrays<KIND>::N;
@@ -234,12 +236,12 @@ struct ZwaveConfig {
     static constexpr int NAR = NAUX > 0 ? (TB - 1) * R + 1 + PA : 0;  // aux ring depth
     static constexpr int AUXPLANE = NAUX * AYX;
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
-    static constexpr int GUARD = round16(LX * R + R);
+    static constexpr int GUARD = round16(LX * R + R + 8);
     static constexpr int STAGE = round16(OXM * OY);  // one output staging plane
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
                                            size_t(NAR) * AUXPLANE + 2 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
-    static_assert(CELLS % NT == 0, "tile must split evenly over the CTA");
+    static_assert(CELLS % (2 * NT) == 0, "tile must split evenly into cell pairs over the CTA");
     static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
     static_assert(LX - 2 * H - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(NT, MINB)
                  const __grid_constant__ PassParams p) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
     constexpr int R = CFG::R, Q = CFG::Q, NR0 = CFG::NR0, H = CFG::H;
-    constexpr int CELLS = CFG::CELLS, CPT = CFG::CPT, OY = CFG::OY;
+    constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA, OY = CFG::OY;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr int AX = CFG::AX, AYX = CFG::AYX, AUXPLANE = CFG::AUXPLANE;
     constexpr int GUARD = CFG::GUARD, STAGE = CFG::STAGE;
@@ -339,17 +341,23 @@ __global__ void __launch_bounds__(NT, MINB)
     bool pend = false;
     int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0;
 
-    // ---- per-thread cell constants (bit i of a mask = cell i of this thread) ----
-    int lcell[CPT], dyv[CPT], ai[CPT], sidx[CPT];
+    // ---- per-thread constants. A thread owns x-PAIRS of cells (2 consecutive x): every
+    //      neighbour access is a 16-byte LDS.128 and the x neighbourhood of a pair comes from
+    //      XA+1 aligned pair loads. Bit 2i+q of a mask = cell q of pair i. ----
+    int lcell[PPT], dyv[PPT], ai[PPT], sidx[PPT];
     uint32_t out_mask = 0;
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-        const int c = tid + NT * i;
+    for (int i = 0; i < PPT; ++i) {
+        const int c = 2 * (tid + NT * i);  // first cell of the pair (even)
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
-        const int dx = min(lx, LX - 1 - lx), dy = min(ly, LY - 1 - ly);
-        dyv[i] = dy;  // warp-uniform (a warp covers part of one tile row)
-        if (dx >= p.hx && dy >= H) out_mask |= 1u << i;
+        const int dy = min(ly, LY - 1 - ly);
+        dyv[i] = dy;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int dx = min(lx + q, LX - 1 - lx - q);
+            if (dx >= p.hx && dy >= H) out_mask |= 1u << (2 * i + q);
+        }
         ai[i] = (ly - AYO) * AX + (lx - AXO);
         sidx[i] = (ly - H) * p.ox + (lx - p.hx);
     }
@@ -367,21 +375,31 @@ __global__ void __launch_bounds__(NT, MINB)
 
         // ghost columns (ghost value instead of the stencil) and in-allocation columns
         uint32_t ghost_mask = 0, ok_mask = 0;
-        int colidx[CPT];  // row offset within a plane (allocated coordinates)
+        int colidx[2 * PPT];  // row offset within a plane (allocated coordinates)
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-            const int xa = xa0 + lcell[i] % LX, ya = ya0 + lcell[i] / LX;
-            if (xa >= 0 && xa < p.X && ya >= 0 && ya < p.Y) ok_mask |= 1u << i;
-            if (xa < R || xa >= R + p.nx || ya < R || ya >= R + p.ny) ghost_mask |= 1u << i;
-            const int cx = min(max(xa, 0), p.X - 1), cy = min(max(ya, 0), p.Y - 1);
-            colidx[i] = cy * p.pitch + p.off + cx;
-        }
+        for (int i = 0; i < PPT; ++i)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int b = 2 * i + q;
+                const int xa = xa0 + (lcell[i] + q) % LX, ya = ya0 + lcell[i] / LX;
+                if (xa >= 0 && xa < p.X && ya >= 0 && ya < p.Y) ok_mask |= 1u << b;
+                if (xa < R || xa >= R + p.nx || ya < R || ya >= R + p.ny) ghost_mask |= 1u << b;
+                const int cx = min(max(xa, 0), p.X - 1), cy = min(max(ya, 0), p.Y - 1);
+                colidx[b] = cy * p.pitch + p.off + cx;
+            }
         const uint32_t col_fix = ghost_mask & ok_mask;
         const bool any_ghost_col = __syncthreads_or(col_fix != 0);
 
         for (int it = 0; it < n_it; ++it, ++g) {
             const int j = ug.za - H + it;  // level-0 plane of this iteration
             __syncthreads();               // previous iteration's smem reads/writes are complete
+#ifdef GIRIH_ZWAVE_TRACE
+            const bool tr = p.trace && blockIdx.x == 0 && (tid == 0 || tid == 32) && g - G0 < 4096;
+#else
+            constexpr bool tr = false;  // build with -DGIRIH_ZWAVE_TRACE for phase clocks
+#endif
+            unsigned long long* trp = tr ? p.trace + ((g - G0) * 2 + (tid == 32)) * 4 : nullptr;
+            if (tr) trp[0] = clock64();
             if (tid == 0) {
                 if (pend) {  // output plane of the previous iteration (staging fenced by writers)
                     tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
@@ -393,8 +411,9 @@ __global__ void __launch_bounds__(NT, MINB)
             }
             mbar_wait(&vbar[g % NR0], (g / NR0) & 1);
             if constexpr (NAUX > 0) mbar_wait(&abar[g % NAR], (g / NAR) & 1);
+            if (tr) trp[1] = clock64();
 
-            double newest[CPT];  // level s-1 at (cell, k_s + R), produced this iteration
+            double2 newest[PPT];  // level s-1 at (pair, k_s + R), produced this iteration
             bool staged = false;
 #pragma unroll
             for (int s = 1; s <= TB; ++s) {
@@ -406,76 +425,133 @@ __global__ void __launch_bounds__(NT, MINB)
                 if (k >= p.Zloc) continue;
                 const int kg = k + p.zoff;
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
-                const double* pl[Q];  // level s-1 planes k-R .. k+R
+                const double2* pl[Q];  // level s-1 planes k-R .. k+R
                 if (s == 1) {
 #pragma unroll
-                    for (int d = 0; d < Q; ++d) pl[d] = ring0 + ((g - 2 * R + d) % NR0) * CELLS;
+                    for (int d = 0; d < Q; ++d)
+                        pl[d] = reinterpret_cast<const double2*>(ring0 + ((g - 2 * R + d) % NR0) * CELLS);
                 } else {
 #pragma unroll
                     for (int d = 0; d < Q; ++d)
-                        pl[d] = ringL + ((s - 2) * Q + (k - R + d + KOFF) % Q) * CELLS;
+                        pl[d] = reinterpret_cast<const double2*>(
+                            ringL + ((s - 2) * Q + (k - R + d + KOFF) % Q) * CELLS);
                 }
-                const double* aux = NAUX > 0 ? auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE : nullptr;
-                const double* uprev_pl = nullptr;  // const25pt: level s-2 at plane k
+                const double2* aux = NAUX > 0 ? reinterpret_cast<const double2*>(
+                                                    auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE)
+                                              : nullptr;
+                const double2* uprev_pl = nullptr;  // const25pt: level s-2 at plane k
                 if constexpr (KIND == K_CONST25) {
-                    if (s == 2) uprev_pl = ring0 + ((g - 2 * R) % NR0) * CELLS;
-                    else if (s > 2) uprev_pl = ringL + ((s - 3) * Q + (k + KOFF) % Q) * CELLS;
+                    if (s == 2)
+                        uprev_pl = reinterpret_cast<const double2*>(ring0 + ((g - 2 * R) % NR0) * CELLS);
+                    else if (s > 2)
+                        uprev_pl = reinterpret_cast<const double2*>(
+                            ringL + ((s - 3) * Q + (k + KOFF) % Q) * CELLS);
                 }
 
-                // (1) stencil for every cell of the valid rows; lanes outside the valid area in
-                //     x compute garbage that no valid cell ever reads (guard rows keep the
-                //     smem reads in bounds)
-                double val[CPT];
+                // (1) stencil for every pair of the valid rows; cells outside the valid area in x
+                //     compute garbage that no valid cell ever reads (guard rows keep the smem
+                //     reads in bounds)
+                double2 val[PPT];
 #pragma unroll
-                for (int i = 0; i < CPT; ++i) {
-                    val[i] = 0.0;
-                    if (dyv[i] < s * R) continue;  // warp-uniform
-                    const int c = lcell[i];
-                    auto V = [&](int dx, int dy, int dz) -> double {
+                for (int i = 0; i < PPT; ++i) {
+                    val[i] = make_double2(0.0, 0.0);
+                    if (dyv[i] < s * R) continue;
+                    const int h2 = lcell[i] >> 1;  // pair index within a plane
+                    // x neighbourhood x = c-XA .. c+1+XA from XA+1 aligned pair loads
+                    double xs[2 * XA + 2];
+#pragma unroll
+                    for (int t = 0; t <= XA; ++t) {
+                        const double2 w = pl[R][h2 - XA / 2 + t];
+                        xs[2 * t] = w.x;
+                        xs[2 * t + 1] = w.y;
+                    }
+                    auto X = [&](int q, int dx) -> double { return xs[q + dx + XA]; };
+                    auto Yp = [&](int dy) -> double2 { return pl[R][h2 + dy * (LX / 2)]; };
+                    auto Zp = [&](int dz) -> double2 {
                         if (dz == R && s > 1) return newest[i];
-                        return pl[dz + R][c + dx + dy * LX];
+                        return pl[dz + R][h2];
                     };
-                    auto Cf = [&](int a) -> double { return aux[a * AYX + ai[i]]; };
-                    double v;
+                    auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
+                    auto comp = [](const double2& v, int q) -> double { return q ? v.y : v.x; };
+                    double out[2];
                     if constexpr (KIND == K_CONST7) {
                         const double c0 = p.cc[0], c1 = p.cc[1];
-                        v = dmul(c0, V(0, 0, 0));
-                        v = dadd(v, dmul(c1, dadd(V(1, 0, 0), V(-1, 0, 0))));
-                        v = dadd(v, dmul(c1, dadd(V(0, 1, 0), V(0, -1, 0))));
-                        v = dadd(v, dmul(c1, dadd(V(0, 0, 1), V(0, 0, -1))));
-                    } else if constexpr (KIND == K_VAR7) {
-                        v = dmul(Cf(0), V(0, 0, 0));
-                        v = dadd(v, dmul(Cf(1), V(1, 0, 0)));
-                        v = dadd(v, dmul(Cf(2), V(-1, 0, 0)));
-                        v = dadd(v, dmul(Cf(3), V(0, 1, 0)));
-                        v = dadd(v, dmul(Cf(4), V(0, -1, 0)));
-                        v = dadd(v, dmul(Cf(5), V(0, 0, 1)));
-                        v = dadd(v, dmul(Cf(6), V(0, 0, -1)));
-                    } else if constexpr (KIND == K_CONST25) {
-                        const double vc = V(0, 0, 0);
-                        double lap = dmul(p.cc[0], vc);
+                        const double2 yp = Yp(1), ym = Yp(-1), zp = Zp(1), zm = Zp(-1);
 #pragma unroll
-                        for (int r = 1; r <= 4; ++r) {
-                            double sr = dadd(V(r, 0, 0), V(-r, 0, 0));
-                            sr = dadd(sr, V(0, r, 0));
-                            sr = dadd(sr, V(0, -r, 0));
-                            sr = dadd(sr, V(0, 0, r));
-                            sr = dadd(sr, V(0, 0, -r));
-                            lap = dadd(lap, dmul(p.cc[r], sr));
+                        for (int q = 0; q < 2; ++q) {
+                            double v = dmul(c0, X(q, 0));
+                            v = dadd(v, dmul(c1, dadd(X(q, 1), X(q, -1))));
+                            v = dadd(v, dmul(c1, dadd(comp(yp, q), comp(ym, q))));
+                            v = dadd(v, dmul(c1, dadd(comp(zp, q), comp(zm, q))));
+                            out[q] = v;
                         }
-                        const double uprev = s == 1 ? Cf(1) : uprev_pl[c];
-                        v = dadd(dsub(dmul(2.0, vc), uprev), dmul(Cf(0), lap));
-                    } else {  // K_VAR25
-                        v = dmul(Cf(0), V(0, 0, 0));
+                    } else if constexpr (KIND == K_VAR7) {
+                        const double2 yp = Yp(1), ym = Yp(-1), zp = Zp(1), zm = Zp(-1);
+                        double2 cf[7];
+#pragma unroll
+                        for (int a = 0; a < 7; ++a) cf[a] = Cp(a);
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            double v = dmul(comp(cf[0], q), X(q, 0));
+                            v = dadd(v, dmul(comp(cf[1], q), X(q, 1)));
+                            v = dadd(v, dmul(comp(cf[2], q), X(q, -1)));
+                            v = dadd(v, dmul(comp(cf[3], q), comp(yp, q)));
+                            v = dadd(v, dmul(comp(cf[4], q), comp(ym, q)));
+                            v = dadd(v, dmul(comp(cf[5], q), comp(zp, q)));
+                            v = dadd(v, dmul(comp(cf[6], q), comp(zm, q)));
+                            out[q] = v;
+                        }
+                    } else if constexpr (KIND == K_CONST25) {
+                        double2 yp[4], ym[4], zp[4], zm[4];
 #pragma unroll
                         for (int r = 1; r <= 4; ++r) {
-                            const int b = 3 * (r - 1);
-                            v = dadd(v, dmul(Cf(b + 1), dadd(V(r, 0, 0), V(-r, 0, 0))));
-                            v = dadd(v, dmul(Cf(b + 2), dadd(V(0, r, 0), V(0, -r, 0))));
-                            v = dadd(v, dmul(Cf(b + 3), dadd(V(0, 0, r), V(0, 0, -r))));
+                            yp[r - 1] = Yp(r);
+                            ym[r - 1] = Yp(-r);
+                            zp[r - 1] = Zp(r);
+                            zm[r - 1] = Zp(-r);
+                        }
+                        const double2 cf = Cp(0);
+                        const double2 up = s == 1 ? Cp(1) : uprev_pl[h2];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const double vc = X(q, 0);
+                            double lap = dmul(p.cc[0], vc);
+#pragma unroll
+                            for (int r = 1; r <= 4; ++r) {
+                                double sr = dadd(X(q, r), X(q, -r));
+                                sr = dadd(sr, comp(yp[r - 1], q));
+                                sr = dadd(sr, comp(ym[r - 1], q));
+                                sr = dadd(sr, comp(zp[r - 1], q));
+                                sr = dadd(sr, comp(zm[r - 1], q));
+                                lap = dadd(lap, dmul(p.cc[r], sr));
+                            }
+                            out[q] = dadd(dsub(dmul(2.0, vc), comp(up, q)), dmul(comp(cf, q), lap));
+                        }
+                    } else {  // K_VAR25
+                        double2 yp[4], ym[4], zp[4], zm[4];
+#pragma unroll
+                        for (int r = 1; r <= 4; ++r) {
+                            yp[r - 1] = Yp(r);
+                            ym[r - 1] = Yp(-r);
+                            zp[r - 1] = Zp(r);
+                            zm[r - 1] = Zp(-r);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            double v = dmul(comp(Cp(0), q), X(q, 0));
+#pragma unroll
+                            for (int r = 1; r <= 4; ++r) {
+                                const int b = 3 * (r - 1);
+                                v = dadd(v, dmul(comp(Cp(b + 1), q), dadd(X(q, r), X(q, -r))));
+                                v = dadd(v, dmul(comp(Cp(b + 2), q),
+                                                 dadd(comp(yp[r - 1], q), comp(ym[r - 1], q))));
+                                v = dadd(v, dmul(comp(Cp(b + 3), q),
+                                                 dadd(comp(zp[r - 1], q), comp(zm[r - 1], q))));
+                            }
+                            out[q] = v;
                         }
                     }
-                    val[i] = v;
+                    val[i] = make_double2(out[0], out[1]);
                 }
                 // (2) ghost cells of level s hold the parity-(t0+s) field's ghosts (block edges
                 //     and ghost planes only: a uniform branch elsewhere)
@@ -483,33 +559,44 @@ __global__ void __launch_bounds__(NT, MINB)
                     const double* ghost = p.ghost[(p.parity0 + s) & 1] + (long long)k * p.plane;
                     const uint32_t fix = plane_ghost ? ok_mask : col_fix;
 #pragma unroll
-                    for (int i = 0; i < CPT; ++i)
-                        if (dyv[i] >= s * R && ((fix >> i) & 1)) val[i] = __ldg(ghost + colidx[i]);
+                    for (int i = 0; i < PPT; ++i) {
+                        if (dyv[i] < s * R) continue;
+                        if ((fix >> (2 * i)) & 1) val[i].x = __ldg(ghost + colidx[2 * i]);
+                        if ((fix >> (2 * i + 1)) & 1) val[i].y = __ldg(ghost + colidx[2 * i + 1]);
+                    }
                 }
                 // (3) results: the level-s ring (s < TB) or the output staging plane (s == TB)
                 if (s < TB) {
-                    double* wr = ringL + ((s - 1) * Q + (k + KOFF) % Q) * CELLS;
+                    double2* wr = reinterpret_cast<double2*>(
+                        ringL + ((s - 1) * Q + (k + KOFF) % Q) * CELLS);
 #pragma unroll
-                    for (int i = 0; i < CPT; ++i) {
+                    for (int i = 0; i < PPT; ++i) {
                         if (dyv[i] < s * R) continue;
-                        wr[lcell[i]] = val[i];
+                        wr[lcell[i] >> 1] = val[i];
                         newest[i] = val[i];
                     }
                 } else if (k >= ug.za && k < ug.zb) {
                     double* stg = stage + (g & 1) * STAGE;
 #pragma unroll
-                    for (int i = 0; i < CPT; ++i)
-                        if ((out_mask >> i) & 1) stg[sidx[i]] = val[i];  // clipped by omap
+                    for (int i = 0; i < PPT; ++i) {
+                        if ((out_mask >> (2 * i)) & 1) stg[sidx[i]] = val[i].x;  // clipped by omap
+                        if ((out_mask >> (2 * i + 1)) & 1) stg[sidx[i] + 1] = val[i].y;
+                    }
                     if (has_penult) {  // final pass only: level TB-1 of the same cells
                         double* pen = p.dst_penult + (long long)k * p.plane;
 #pragma unroll
-                        for (int i = 0; i < CPT; ++i)
-                            if ((out_mask >> i) & 1 && !((ghost_mask >> i) & 1))
-                                pen[colidx[i]] = pl[R][lcell[i]];
+                        for (int i = 0; i < PPT; ++i) {
+                            const double2 c2 = pl[R][lcell[i] >> 1];
+                            const int b = 2 * i;
+                            if ((out_mask >> b) & 1 && !((ghost_mask >> b) & 1)) pen[colidx[b]] = c2.x;
+                            if ((out_mask >> (b + 1)) & 1 && !((ghost_mask >> (b + 1)) & 1))
+                                pen[colidx[b + 1]] = c2.y;
+                        }
                     }
                     staged = true;
                 }
             }
+            if (tr) trp[2] = clock64();
             // hand the staged output plane to the async proxy; thread 0 stores it next iteration
             if (staged) {
                 fence_proxy_async_smem();
@@ -524,6 +611,7 @@ __global__ void __launch_bounds__(NT, MINB)
             // the store issued at the top of this iteration must finish reading its staging
             // plane before the next iteration overwrites that plane
             if (tid == 0) bulk_wait_read_all();
+            if (tr) trp[3] = clock64();
         }
     }
     __syncthreads();
