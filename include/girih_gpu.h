@@ -65,7 +65,8 @@ typedef struct {
     int ngpus;     /* >1: z-slab decomposition over devices [device, device+ngpus) */
     int exact;     /* 1 = bitwise mode (no FMA contraction); 0 is rejected */
     int device;    /* CUDA device ordinal of the (first) GPU */
-    int graphs;    /* 1 = capture the pass sequence of a step call in a CUDA graph */
+    int graphs;    /* >= 0: replay each step's pass sequence as a cached CUDA graph (single-
+                      stream handles); -1 = launch passes individually */
     int reserved;
 } girih_gpu_config;
 

@@ -366,6 +366,13 @@ struct DevBuf {
     }
 };
 
+struct StepStats {
+    int n_launches = 0;
+    double pass_s = 0;
+    long long computed = 0;
+    int grid = 0, zchunks = 0, variant = -1, tb_used = 0;
+};
+
 // One z-slab: local planes [0, Zloc) hold global allocated planes [zoff, zoff + Zloc).
 struct Slab {
     int gidx = 0, gcount = 1;  // position of this slab in the global decomposition
@@ -406,6 +413,14 @@ struct Handle {
         CUtensorMap map;
     };
     std::vector<std::unique_ptr<MapEntry>> maps;
+    struct GraphEntry {
+        long long parity = 0, steps = 0;
+        int tb = 0, variant = 0, zchunks = 0;
+        bool timed = false;
+        cudaGraphExec_t exec = nullptr;
+        StepStats st;
+    };
+    std::vector<GraphEntry> graphs;
 
     size_t plane_elems() const { return size_t(pitch) * Y; }
     size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
@@ -631,7 +646,16 @@ void sync_all(Handle& h) {
     GCHECK(cudaSetDevice(h.slabs[0].device));
 }
 
+// captured pass sequences bake in buffer pointers and scalar coefficients: drop them whenever
+// the state is (re)loaded
+void drop_graphs(Handle& h) {
+    for (auto& g : h.graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    h.graphs.clear();
+}
+
 void upload_state(Handle& h, const girih_state_view& v) {
+    drop_graphs(h);
     if (!v.u || !v.v) throw_err(GIRIH_EINVAL, "state view lacks u/v");
     if (v.n_coeffs != h.nc) throw_err(GIRIH_EINVAL, "coefficient field count does not match kind");
     for (int c = 0; c < h.nc; ++c)
@@ -659,6 +683,7 @@ void upload_state(Handle& h, const girih_state_view& v) {
 }
 
 void init_state_device(Handle& h, uint64_t seed, int remap) {
+    drop_graphs(h);
     const KindInfo& ki = kind_info(h.kind);
     double coeff_scale = 1.0;
     if (h.kind == K_VAR7) coeff_scale = 0.14;
@@ -720,10 +745,15 @@ const CUtensorMap& tensor_map(Handle& h, int slab, const double* base, int narr,
 // keep every tile in flight within ~one chunk of its neighbours (halo rows stay in L2) and
 // balance the load; each chunk re-streams 2H extra level-0 planes (L2 hits) and recomputes
 // 2(TB-s)R planes of level s, so chunks grow with the fused depth.
-int choose_zchunks(int nzl, int H, int ncoeff) {
+int choose_zchunks(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
     // coefficient-heavy kinds: each chunk boundary re-streams (TB-1)R coefficient planes that
     // no longer sit in L2 (16.8 MB per 512^2 plane for var7pt), so their chunks are longer
-    const int len = ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
+    int len = ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
+    // small grids: shorten chunks until there are >= 2 units per resident CTA (latency-bound
+    // otherwise: few CTAs, each waiting on its own TMA pipeline)
+    const int min_len = std::max(4, 2 * H);
+    while (len > min_len && (long long)tiles_xy * ((nzl + len - 1) / len) < 2LL * grid)
+        len = std::max(min_len, len / 2);
     return std::max(1, (nzl + len - 1) / len);
 }
 
@@ -731,6 +761,18 @@ struct LaunchInfo {
     int grid = 0, zchunks = 0;
     long long computed_lups = 0;
 };
+
+// CTAs per SM of a variant (queried once per process and variant)
+int occupancy_of(const Variant* var) {
+    static std::map<const Variant*, int> cache;
+    auto it = cache.find(var);
+    if (it != cache.end()) return it->second;
+    int occ = 0;
+    GCHECK(var->occupancy(&occ));
+    if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
+    cache[var] = occ;
+    return occ;
+}
 
 // Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
 PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_index,
@@ -766,12 +808,10 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.zout_lo = s.zout_lo;
     p.zout_hi = s.zout_hi;
     const int nzl = s.zout_hi - s.zout_lo;
-    int occ = 1;
-    GCHECK(var->occupancy(&occ));
-    if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
+    int occ = occupancy_of(var);
     const int max_grid = h.sm_count * occ;
     const int txy = p.tiles_x * p.tiles_y;
-    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl) : choose_zchunks(nzl, H, h.nc);
+    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl) : choose_zchunks(nzl, H, h.nc, txy, max_grid);
     p.zc_len = (nzl + p.nzc - 1) / p.nzc;
     p.nzc = (nzl + p.zc_len - 1) / p.zc_len;
     p.units = txy * p.nzc;
@@ -801,12 +841,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
 // Out-of-namespace helpers that need PassParams parity (kept separate for clarity)
 namespace {
 
-struct StepStats {
-    int n_launches = 0;
-    double pass_s = 0;
-    long long computed = 0;
-    int grid = 0, zchunks = 0, variant = -1, tb_used = 0;
-};
+
 
 void exchange_halos(Handle& h, int buf) {
     const size_t pe = h.plane_elems();
@@ -872,6 +907,48 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             h.ev.push_back(e);
         }
     }
+    // CUDA graph of the whole pass sequence (single-stream handles): replayed whenever the
+    // same (t0 parity, steps, configuration) comes back, e.g. every bench / solver step
+    const bool use_graph = h.cfg.graphs >= 0 && h.slabs.size() == 1 && h.nranks == 1 &&
+                           !std::getenv("GIRIH_TRACE") && !std::getenv("GIRIH_NO_GRAPHS");
+    Handle::GraphEntry* ge = nullptr;
+    if (use_graph) {
+        for (auto& e : h.graphs)
+            if (e.parity == parity_of(h.t_current) && e.steps == steps && e.tb == tb &&
+                e.variant == h.cfg.variant && e.zchunks == h.cfg.zchunks && e.timed == time_passes)
+                ge = &e;
+        if (ge) {
+            GCHECK(cudaSetDevice(h.slabs[0].device));
+            GCHECK(cudaGraphLaunch(ge->exec, h.slabs[0].stream));
+            st = ge->st;
+            h.t_current += steps;
+            if (time_passes) {
+                sync_all(h);
+                st.pass_s = 0;
+                for (int i = 0; i < st.n_launches; ++i) {
+                    float ms = 0;
+                    GCHECK(cudaEventElapsedTime(&ms, h.ev[2 * i], h.ev[2 * i + 1]));
+                    st.pass_s += ms * 1e-3;
+                }
+            }
+            return st;
+        }
+        GCHECK(cudaSetDevice(h.slabs[0].device));
+        GCHECK(cudaStreamBeginCapture(h.slabs[0].stream, cudaStreamCaptureModeThreadLocal));
+    }
+    struct CaptureGuard {  // never leave the stream capturing when a pass fails to launch
+        cudaStream_t st;
+        bool active;
+        ~CaptureGuard() {
+            if (active) {
+                cudaGraph_t gr = nullptr;
+                cudaStreamEndCapture(st, &gr);
+                if (gr) cudaGraphDestroy(gr);
+                cudaGetLastError();
+            }
+        }
+    } guard{h.slabs[0].stream, use_graph};
+    const long long t_begin = h.t_current;
     long long t = h.t_current;
     int pi = 0;
     for (const Pass& ps : plan) {
@@ -896,9 +973,13 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             const CUtensorMap& omap = tensor_map(h, int(g), s.buf[ps.dst]->p, 1, p.ox,
                                                  var->ly - 2 * ps.tb * h.R, 1);
             GCHECK(cudaMemsetAsync(p.work, 0, sizeof(int), s.stream));
-            if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi], s.stream));
+            // inside a stream capture a plain record only orders streams: record as graph nodes
+            const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+            if (time_passes && g == 0)
+                GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
             GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
-            if (time_passes && g == 0) GCHECK(cudaEventRecord(h.ev[2 * pi + 1], s.stream));
+            if (time_passes && g == 0)
+                GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
             if (p.trace) {  // debug: dump CTA 0's phase clocks of this pass
                 std::vector<unsigned long long> tv(4096 * 8);
                 GCHECK(cudaMemcpyAsync(tv.data(), p.trace, tv.size() * 8, cudaMemcpyDeviceToHost,
@@ -926,6 +1007,24 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         ++pi;
     }
     h.t_current = t;
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        guard.active = false;
+        GCHECK(cudaStreamEndCapture(h.slabs[0].stream, &graph));
+        Handle::GraphEntry e{};
+        e.parity = parity_of(t_begin);
+        e.steps = steps;
+        e.tb = tb;
+        e.variant = h.cfg.variant;
+        e.zchunks = h.cfg.zchunks;
+        e.timed = time_passes;
+        e.st = st;
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        GCHECK(ie);
+        h.graphs.push_back(e);
+        GCHECK(cudaGraphLaunch(e.exec, h.slabs[0].stream));
+    }
     if (time_passes) {
         sync_all(h);
         for (int i = 0; i < pi; ++i) {
@@ -966,6 +1065,8 @@ void destroy(Handle* h) {
         if (s.done) cudaEventDestroy(s.done);
     }
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+    for (auto& g : h->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (Slab& s : h->slabs) {
         for (auto& b : s.buf) b.reset();
         s.cblock.reset();

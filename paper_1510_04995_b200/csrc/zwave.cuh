@@ -220,14 +220,18 @@ template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1>
 struct ZwaveConfig {
     static constexpr int R = KindTraits<KIND>::R;
     static constexpr int Q = 2 * R + 1;     // z window of one level
-    static constexpr int NR0 = Q + P;       // level-0 TMA ring depth
+    // z neighbours come from per-thread register queues; smem only holds the centre planes
+    // that other threads read for x/y neighbours: R+1 planes per computed level (written R
+    // iterations before they are read) and R+1+P for the TMA-fed level 0
+    static constexpr int QL = R + 1;        // level-s (s >= 1) centre-plane ring depth
+    static constexpr int NR0 = R + 1 + P;   // level-0 TMA ring depth
     static constexpr int H = TB * R;        // halo of the loaded tile
     static constexpr int OY = LY - 2 * H;   // output tile height (x: runtime, halo H or H+1)
     static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
     static constexpr int PPT = CELLS / (2 * NT);  // x-pairs of cells per thread
     static constexpr int XA = 2 * ((R + 1) / 2);  // pair-aligned x reach (R=1: 2, R=4: 4)
-    static constexpr int NRING = NR0 + (TB - 1) * Q;
+    static constexpr int NRING = NR0 + (TB - 1) * QL;
     // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
     static constexpr int NAUX = AuxArrays<KIND>::N;
     static constexpr int AXO = R & ~1, AYO = R;
@@ -258,21 +262,21 @@ __global__ void __launch_bounds__(NT, MINB)
                  const __grid_constant__ CUtensorMap omap,  // output: interior of dst_final
                  const __grid_constant__ PassParams p) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
-    constexpr int R = CFG::R, Q = CFG::Q, NR0 = CFG::NR0, H = CFG::H;
+    constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
     constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA, OY = CFG::OY;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr int AX = CFG::AX, AYX = CFG::AYX, AUXPLANE = CFG::AUXPLANE;
     constexpr int GUARD = CFG::GUARD, STAGE = CFG::STAGE;
     constexpr uint32_t PLANE_BYTES = CELLS * sizeof(double);
     constexpr uint32_t AUX_BYTES = AUXPLANE * sizeof(double);
-    constexpr int KOFF = Q * 4096;  // keeps ring indices of planes below 0 non-negative
+    constexpr int KOFF = QL * 4096;  // keeps ring indices of planes below 0 non-negative
     // stream counters start at a common multiple of the ring depths (first phase parity 0)
     constexpr uint32_t G0 = 8u * NR0 * (NAR > 0 ? NAR : 1);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring0 = reinterpret_cast<double*>(smem_raw) + GUARD;
-    double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*Q*CELLS
-    double* auxr = ringL + (TB - 1) * Q * CELLS;   // aux planes: NAR x [NAUX][AY][AX]
+    double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*QL*CELLS
+    double* auxr = ringL + (TB - 1) * QL * CELLS;  // aux planes: NAR x [NAUX][AY][AX]
     double* stage = auxr + NAR * AUXPLANE + GUARD; // 2 output staging planes [OY][ox]
     uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 2 * STAGE);
     uint64_t* abar = vbar + NR0;
@@ -362,6 +366,14 @@ __global__ void __launch_bounds__(NT, MINB)
         sidx[i] = (ly - H) * p.ox + (lx - p.hx);
     }
     const bool has_penult = p.dst_penult != nullptr;
+    // per-thread z queues: zq[L][pair][d] = level L at plane (newest_L - 2R + d), d = 0..2R-1
+    double2 zq[TB][PPT][2 * R];
+#pragma unroll
+    for (int L = 0; L < TB; ++L)
+#pragma unroll
+        for (int i = 0; i < PPT; ++i)
+#pragma unroll
+            for (int d = 0; d < 2 * R; ++d) zq[L][i][d] = make_double2(0.0, 0.0);
 
     __syncthreads();  // uq[0] visible
     uint32_t g = G0;  // consumer's global element index
@@ -413,7 +425,21 @@ __global__ void __launch_bounds__(NT, MINB)
             if constexpr (NAUX > 0) mbar_wait(&abar[g % NAR], (g / NAR) & 1);
             if (tr) trp[1] = clock64();
 
+            // level-0 newest plane j into the level-0 z queue input (one LDS.128 per pair)
             double2 newest[PPT];  // level s-1 at (pair, k_s + R), produced this iteration
+            {
+                const double2* pj = reinterpret_cast<const double2*>(ring0 + (g % NR0) * CELLS);
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) newest[i] = pj[lcell[i] >> 1];
+            }
+            // value of level L at its newest plane (j - L R) this iteration; the z queues advance
+            // by one plane EVERY iteration so zq[L] always holds planes j-LR-2R .. j-LR-1 (entries
+            // of planes a level did not compute are never read by a valid cell)
+            double2 fresh[TB][PPT];
+#pragma unroll
+            for (int L = 0; L < TB; ++L)
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) fresh[L][i] = L == 0 ? newest[i] : make_double2(0.0, 0.0);
             bool staged = false;
 #pragma unroll
             for (int s = 1; s <= TB; ++s) {
@@ -425,28 +451,13 @@ __global__ void __launch_bounds__(NT, MINB)
                 if (k >= p.Zloc) continue;
                 const int kg = k + p.zoff;
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
-                const double2* pl[Q];  // level s-1 planes k-R .. k+R
-                if (s == 1) {
-#pragma unroll
-                    for (int d = 0; d < Q; ++d)
-                        pl[d] = reinterpret_cast<const double2*>(ring0 + ((g - 2 * R + d) % NR0) * CELLS);
-                } else {
-#pragma unroll
-                    for (int d = 0; d < Q; ++d)
-                        pl[d] = reinterpret_cast<const double2*>(
-                            ringL + ((s - 2) * Q + (k - R + d + KOFF) % Q) * CELLS);
-                }
+                // centre plane k of level s-1 (x/y neighbours, other threads' values)
+                const double2* pc = reinterpret_cast<const double2*>(
+                    s == 1 ? ring0 + ((g - R) % NR0) * CELLS
+                           : ringL + ((s - 2) * QL + (k + KOFF) % QL) * CELLS);
                 const double2* aux = NAUX > 0 ? reinterpret_cast<const double2*>(
                                                     auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE)
                                               : nullptr;
-                const double2* uprev_pl = nullptr;  // const25pt: level s-2 at plane k
-                if constexpr (KIND == K_CONST25) {
-                    if (s == 2)
-                        uprev_pl = reinterpret_cast<const double2*>(ring0 + ((g - 2 * R) % NR0) * CELLS);
-                    else if (s > 2)
-                        uprev_pl = reinterpret_cast<const double2*>(
-                            ringL + ((s - 3) * Q + (k + KOFF) % Q) * CELLS);
-                }
 
                 // (1) stencil for every pair of the valid rows; cells outside the valid area in x
                 //     compute garbage that no valid cell ever reads (guard rows keep the smem
@@ -461,15 +472,17 @@ __global__ void __launch_bounds__(NT, MINB)
                     double xs[2 * XA + 2];
 #pragma unroll
                     for (int t = 0; t <= XA; ++t) {
-                        const double2 w = pl[R][h2 - XA / 2 + t];
+                        const double2 w = pc[h2 - XA / 2 + t];
                         xs[2 * t] = w.x;
                         xs[2 * t + 1] = w.y;
                     }
                     auto X = [&](int q, int dx) -> double { return xs[q + dx + XA]; };
-                    auto Yp = [&](int dy) -> double2 { return pl[R][h2 + dy * (LX / 2)]; };
+                    auto Yp = [&](int dy) -> double2 { return pc[h2 + dy * (LX / 2)]; };
+                    // z neighbours of level s-1 at planes k-R .. k+R: register queue zq[s-1]
+                    // holds k-R .. k+R-1 (oldest first), the newest (k+R) was produced above
                     auto Zp = [&](int dz) -> double2 {
-                        if (dz == R && s > 1) return newest[i];
-                        return pl[dz + R][h2];
+                        if (dz == R) return newest[i];
+                        return zq[s - 1][i][dz + R];
                     };
                     auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
                     auto comp = [](const double2& v, int q) -> double { return q ? v.y : v.x; };
@@ -502,16 +515,16 @@ __global__ void __launch_bounds__(NT, MINB)
                             out[q] = v;
                         }
                     } else if constexpr (KIND == K_CONST25) {
-                        double2 yp[4], ym[4], zp[4], zm[4];
+                        double2 yp[4], ym[4];
 #pragma unroll
                         for (int r = 1; r <= 4; ++r) {
                             yp[r - 1] = Yp(r);
                             ym[r - 1] = Yp(-r);
-                            zp[r - 1] = Zp(r);
-                            zm[r - 1] = Zp(-r);
                         }
                         const double2 cf = Cp(0);
-                        const double2 up = s == 1 ? Cp(1) : uprev_pl[h2];
+                        // level s-2 at plane k: t0-1 from the aux ring (s = 1), else the oldest
+                        // entry of level s-2's z queue (before this iteration's shift)
+                        const double2 up = s == 1 ? Cp(1) : zq[s >= 2 ? s - 2 : 0][i][0];
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
                             const double vc = X(q, 0);
@@ -521,20 +534,18 @@ __global__ void __launch_bounds__(NT, MINB)
                                 double sr = dadd(X(q, r), X(q, -r));
                                 sr = dadd(sr, comp(yp[r - 1], q));
                                 sr = dadd(sr, comp(ym[r - 1], q));
-                                sr = dadd(sr, comp(zp[r - 1], q));
-                                sr = dadd(sr, comp(zm[r - 1], q));
+                                sr = dadd(sr, comp(Zp(r), q));
+                                sr = dadd(sr, comp(Zp(-r), q));
                                 lap = dadd(lap, dmul(p.cc[r], sr));
                             }
                             out[q] = dadd(dsub(dmul(2.0, vc), comp(up, q)), dmul(comp(cf, q), lap));
                         }
                     } else {  // K_VAR25
-                        double2 yp[4], ym[4], zp[4], zm[4];
+                        double2 yp[4], ym[4];
 #pragma unroll
                         for (int r = 1; r <= 4; ++r) {
                             yp[r - 1] = Yp(r);
                             ym[r - 1] = Yp(-r);
-                            zp[r - 1] = Zp(r);
-                            zm[r - 1] = Zp(-r);
                         }
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
@@ -546,7 +557,7 @@ __global__ void __launch_bounds__(NT, MINB)
                                 v = dadd(v, dmul(comp(Cp(b + 2), q),
                                                  dadd(comp(yp[r - 1], q), comp(ym[r - 1], q))));
                                 v = dadd(v, dmul(comp(Cp(b + 3), q),
-                                                 dadd(comp(zp[r - 1], q), comp(zm[r - 1], q))));
+                                                 dadd(comp(Zp(r), q), comp(Zp(-r), q))));
                             }
                             out[q] = v;
                         }
@@ -565,12 +576,14 @@ __global__ void __launch_bounds__(NT, MINB)
                         if ((fix >> (2 * i + 1)) & 1) val[i].y = __ldg(ghost + colidx[2 * i + 1]);
                     }
                 }
-                // (3) results: the level-s ring (s < TB) or the output staging plane (s == TB)
+                // (3) results: the level-s centre ring + z queue input (s < TB) or the output
+                //     staging plane (s == TB)
                 if (s < TB) {
                     double2* wr = reinterpret_cast<double2*>(
-                        ringL + ((s - 1) * Q + (k + KOFF) % Q) * CELLS);
+                        ringL + ((s - 1) * QL + (k + KOFF) % QL) * CELLS);
 #pragma unroll
                     for (int i = 0; i < PPT; ++i) {
+                        fresh[s < TB ? s : 0][i] = val[i];
                         if (dyv[i] < s * R) continue;
                         wr[lcell[i] >> 1] = val[i];
                         newest[i] = val[i];
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(NT, MINB)
                         double* pen = p.dst_penult + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
-                            const double2 c2 = pl[R][lcell[i] >> 1];
+                            const double2 c2 = zq[TB - 1][i][R];  // level TB-1 at plane k
                             const int b = 2 * i;
                             if ((out_mask >> b) & 1 && !((ghost_mask >> b) & 1)) pen[colidx[b]] = c2.x;
                             if ((out_mask >> (b + 1)) & 1 && !((ghost_mask >> (b + 1)) & 1))
@@ -594,6 +607,16 @@ __global__ void __launch_bounds__(NT, MINB)
                         }
                     }
                     staged = true;
+                }
+            }
+            // advance every level's z queue by one plane
+#pragma unroll
+            for (int L = 0; L < TB; ++L) {
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) {
+#pragma unroll
+                    for (int d = 0; d + 1 < 2 * R; ++d) zq[L][i][d] = zq[L][i][d + 1];
+                    zq[L][i][2 * R - 1] = fresh[L][i];
                 }
             }
             if (tr) trp[2] = clock64();

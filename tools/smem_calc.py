@@ -6,13 +6,13 @@ r16 = lambda n: (n + 15) // 16 * 16
 
 
 def smem(kind, tb, lx, ly, nt, p, pa):
-    R = RAD[kind]; Q = 2 * R + 1; NR0 = Q + p; H = tb * R
+    R = RAD[kind]; QL = R + 1; NR0 = R + 1 + p; H = tb * R
     OY = ly - 2 * H; OXM = lx - 2 * H; CELLS = lx * ly
-    NRING = NR0 + (tb - 1) * Q
+    NRING = NR0 + (tb - 1) * QL
     NAUX = NAUXA[kind]; AXO = R & ~1; AX = lx - 2 * AXO; AY = ly - 2 * R
     NAR = (tb - 1) * R + 1 + pa if NAUX else 0
     AUXPLANE = NAUX * AX * AY
-    GUARD = r16(lx * R + R); STAGE = r16(OXM * OY)
+    GUARD = r16(lx * R + R + 8); STAGE = r16(OXM * OY)
     d = 2 * GUARD + NRING * CELLS + NAR * AUXPLANE + 2 * STAGE
     return d * 8 + 8 * (NR0 + NAR)
 
