@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgirih_gpu.so")
+# GIRIH_LIB overrides the library path (A/B measurements of two builds in one process)
+LIB_PATH = os.environ.get("GIRIH_LIB") or os.path.join(HERE, "libgirih_gpu.so")
 
 GIRIH_OK = 0
 GIRIH_EINVAL = -1

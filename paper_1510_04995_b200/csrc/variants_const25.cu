@@ -6,6 +6,7 @@ namespace girih_gpu {
 
 const Variant kVariantsConst25[] = {
     GIRIH_VARIANT(K_CONST25, 1, 64, 16, 128, 1, 1, 2),
+    GIRIH_VARIANT(K_CONST25, 1, 128, 16, 256, 1, 1, 1),
     GIRIH_VARIANT(K_CONST25, 1, 64, 16, 512, 1, 1, 1),
     GIRIH_VARIANT(K_CONST25, 1, 32, 32, 512, 2, 1, 1),
     GIRIH_VARIANT(K_CONST25, 1, 64, 24, 384, 2, 1, 1),

@@ -136,6 +136,9 @@ __device__ __forceinline__ void tma_store_plane(const CUtensorMap* map, const vo
 __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read_but1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -197,12 +200,18 @@ __device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int s
 
 // advance within / across units; the drawing cursor (V producer) fetches new unit ids
 template <int H, bool DRAW>
-__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, volatile int* uq) {
+__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, volatile int* uq,
+                                            int* drawn) {
     if (++c.it >= c.n_it) {
         int next;
         if (DRAW) {
-            next = gridDim.x + atomicAdd(p.work, 1);
-            if (next > p.units) next = p.units;
+            // the id drawn at the start of this unit; draw the one after it now, so the atomic's
+            // latency hides behind a whole unit instead of stalling the producer warp
+            next = *drawn;
+            if (next < p.units) {
+                const int d = int(gridDim.x) + atomicAdd(p.work, 1);
+                *drawn = d < p.units ? d : p.units;
+            }
             uq[(c.seq + 1) % UQ] = next;
         } else {
             next = uq[(c.seq + 1) % UQ];
@@ -243,7 +252,7 @@ struct ZwaveConfig {
     static constexpr int GUARD = round16(LX * R + R + 8);
     static constexpr int STAGE = round16(OXM * OY);  // one output staging plane
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
-                                           size_t(NAR) * AUXPLANE + 2 * size_t(STAGE);
+                                           size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
     static_assert(CELLS % (2 * NT) == 0, "tile must split evenly into cell pairs over the CTA");
     static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
@@ -277,8 +286,8 @@ __global__ void __launch_bounds__(NT, MINB)
     double* ring0 = reinterpret_cast<double*>(smem_raw) + GUARD;
     double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*QL*CELLS
     double* auxr = ringL + (TB - 1) * QL * CELLS;  // aux planes: NAR x [NAUX][AY][AX]
-    double* stage = auxr + NAR * AUXPLANE + GUARD; // 2 output staging planes [OY][ox]
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 2 * STAGE);
+    double* stage = auxr + NAR * AUXPLANE + GUARD; // 3 output staging planes [OY][ox]
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 3 * STAGE);
     uint64_t* abar = vbar + NR0;
 
     const int tid = threadIdx.x;
@@ -294,6 +303,7 @@ __global__ void __launch_bounds__(NT, MINB)
     __shared__ int uq[UQ];
     Cursor vcur{}, acur{};
     uint32_t vnext = G0, anext = G0;
+    int drawn = 0;  // producer: next unit id, drawn one unit ahead
     auto issue_v = [&]() {
         if (vcur.u >= p.units) return;
         const int j = vcur.ug.za - H + vcur.it;
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(NT, MINB)
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
         tma_load_plane(ring0 + slot * CELLS, &vmap, xd, yd, j, &vbar[slot]);
         ++vnext;
-        cursor_next<H, true>(vcur, p, uq);
+        cursor_next<H, true>(vcur, p, uq, &drawn);
     };
     auto issue_a = [&]() {
         if constexpr (NAUX > 0) {
@@ -317,7 +327,7 @@ __global__ void __launch_bounds__(NT, MINB)
                 // the phase without moving data
                 mbar_arrive(&abar[slot]);
                 ++anext;
-                cursor_next<H, false>(acur, p, uq);
+                cursor_next<H, false>(acur, p, uq, nullptr);
                 return;
             }
             mbar_arrive_expect_tx(&abar[slot], AUX_BYTES);
@@ -329,20 +339,26 @@ __global__ void __launch_bounds__(NT, MINB)
                 tma_load_4d(dst, &cmap, xd, yd, k1, 0, &abar[slot]);
             }
             ++anext;
-            cursor_next<H, false>(acur, p, uq);
+            cursor_next<H, false>(acur, p, uq, nullptr);
         }
     };
     static_assert(P >= PA, "the V producer draws units and must lead the aux producer");
     if (tid == 0) {
         const int u0 = blockIdx.x < p.units ? int(blockIdx.x) : p.units;
         uq[0] = u0;
+        if (u0 < p.units) {
+            const int d = int(gridDim.x) + atomicAdd(p.work, 1);
+            drawn = d < p.units ? d : p.units;
+        } else {
+            drawn = p.units;
+        }
         cursor_set<H>(vcur, p, 0, u0);
         cursor_set<H>(acur, p, 0, u0);
         for (int e = 0; e < P; ++e) issue_v();
         for (int e = 0; e < PA; ++e) issue_a();
     }
     // output store pending from the previous iteration (thread 0)
-    bool pend = false;
+    bool pend = false, stored_now = false;
     int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0;
 
     // ---- per-thread constants. A thread owns x-PAIRS of cells (2 consecutive x): every
@@ -413,10 +429,12 @@ __global__ void __launch_bounds__(NT, MINB)
             unsigned long long* trp = tr ? p.trace + ((g - G0) * 2 + (tid == 32)) * 4 : nullptr;
             if (tr) trp[0] = clock64();
             if (tid == 0) {
+                stored_now = false;
                 if (pend) {  // output plane of the previous iteration (staging fenced by writers)
                     tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
                     bulk_commit();
                     pend = false;
+                    stored_now = true;
                 }
                 issue_v();
                 issue_a();
@@ -441,6 +459,9 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) fresh[L][i] = L == 0 ? newest[i] : make_double2(0.0, 0.0);
             bool staged = false;
+            int ring_slot[TB];  // centre-ring slot each level writes this iteration (-1: none)
+#pragma unroll
+            for (int L = 0; L < TB; ++L) ring_slot[L] = -1;
 #pragma unroll
             for (int s = 1; s <= TB; ++s) {
                 const int k = j - s * R;  // plane of level s
@@ -465,8 +486,8 @@ __global__ void __launch_bounds__(NT, MINB)
                 double2 val[PPT];
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
-                    val[i] = make_double2(0.0, 0.0);
-                    if (dyv[i] < s * R) continue;
+                    // every pair computes (straight-line code the compiler can interleave);
+                    // rows outside the level-s valid area produce values no valid cell reads
                     const int h2 = lcell[i] >> 1;  // pair index within a plane
                     // x neighbourhood x = c-XA .. c+1+XA from XA+1 aligned pair loads
                     double xs[2 * XA + 2];
@@ -579,17 +600,16 @@ __global__ void __launch_bounds__(NT, MINB)
                 // (3) results: the level-s centre ring + z queue input (s < TB) or the output
                 //     staging plane (s == TB)
                 if (s < TB) {
-                    double2* wr = reinterpret_cast<double2*>(
-                        ringL + ((s - 1) * QL + (k + KOFF) % QL) * CELLS);
+                    // the centre-ring store is deferred to the end of the iteration so that
+                    // the loads of every level can be scheduled ahead of it
+                    ring_slot[s < TB ? s : 0] = (k + KOFF) % QL;
 #pragma unroll
                     for (int i = 0; i < PPT; ++i) {
                         fresh[s < TB ? s : 0][i] = val[i];
-                        if (dyv[i] < s * R) continue;
-                        wr[lcell[i] >> 1] = val[i];
                         newest[i] = val[i];
                     }
                 } else if (k >= ug.za && k < ug.zb) {
-                    double* stg = stage + (g & 1) * STAGE;
+                    double* stg = stage + (g % 3) * STAGE;
 #pragma unroll
                     for (int i = 0; i < PPT; ++i) {
                         if ((out_mask >> (2 * i)) & 1) stg[sidx[i]] = val[i].x;  // clipped by omap
@@ -608,6 +628,15 @@ __global__ void __launch_bounds__(NT, MINB)
                     }
                     staged = true;
                 }
+            }
+            // deferred centre-ring stores of levels 1..TB-1 (read by other threads from the
+            // next iteration on, behind the barrier)
+#pragma unroll
+            for (int L = 1; L < TB; ++L) {
+                if (ring_slot[L] < 0) continue;
+                double2* wr = reinterpret_cast<double2*>(ringL + ((L - 1) * QL + ring_slot[L]) * CELLS);
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) wr[lcell[i] >> 1] = fresh[L][i];
             }
             // advance every level's z queue by one plane
 #pragma unroll
@@ -628,12 +657,17 @@ __global__ void __launch_bounds__(NT, MINB)
                     pend_x = ug.tx * p.ox;
                     pend_y = ug.ty * OY;
                     pend_z = j - H - p.zout_lo;
-                    pend_b = int(g & 1);
+                    pend_b = int(g % 3);
                 }
             }
-            // the store issued at the top of this iteration must finish reading its staging
-            // plane before the next iteration overwrites that plane
-            if (tid == 0) bulk_wait_read_all();
+            // three staging planes: the plane the next iteration writes was handed to the store
+            // issued two iterations ago, so only that older store must have finished reading
+            if (tid == 0) {
+                if (stored_now)
+                    bulk_wait_read_but1();  // the store issued this iteration may stay in flight
+                else
+                    bulk_wait_read_all();
+            }
             if (tr) trp[3] = clock64();
         }
     }

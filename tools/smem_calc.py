@@ -13,7 +13,7 @@ def smem(kind, tb, lx, ly, nt, p, pa):
     NAR = (tb - 1) * R + 1 + pa if NAUX else 0
     AUXPLANE = NAUX * AX * AY
     GUARD = r16(lx * R + R + 8); STAGE = r16(OXM * OY)
-    d = 2 * GUARD + NRING * CELLS + NAR * AUXPLANE + 2 * STAGE
+    d = 2 * GUARD + NRING * CELLS + NAR * AUXPLANE + 3 * STAGE
     return d * 8 + 8 * (NR0 + NAR)
 
 
