@@ -6,8 +6,7 @@ namespace girih_gpu {
 
 const Variant kVariantsVar7[] = {
     GIRIH_VARIANT(K_VAR7, 1, 64, 8, 128, 3, 1, 3),
-    GIRIH_VARIANT(K_VAR7, 1, 128, 8, 128, 3, 1, 1),
-    GIRIH_VARIANT(K_VAR7, 1, 64, 8, 256, 3, 1, 2),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 8, 64, 3, 1, 3),
     GIRIH_VARIANT(K_VAR7, 1, 64, 16, 256, 4, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 32, 16, 256, 2, 1, 2),
     GIRIH_VARIANT(K_VAR7, 2, 32, 16, 128, 2, 1, 2),
