@@ -6,10 +6,8 @@ namespace girih_gpu {
 
 const Variant kVariantsConst25[] = {
     GIRIH_VARIANT(K_CONST25, 1, 64, 16, 128, 1, 1, 2),
-    GIRIH_VARIANT(K_CONST25, 1, 128, 16, 256, 1, 1, 1),
-    GIRIH_VARIANT(K_CONST25, 1, 64, 16, 512, 1, 1, 1),
-    GIRIH_VARIANT(K_CONST25, 1, 32, 32, 512, 2, 1, 1),
-    GIRIH_VARIANT(K_CONST25, 1, 64, 24, 384, 2, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 512, 1, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 24, 384, 1, 1, 1),
     GIRIH_VARIANT(K_CONST25, 2, 32, 32, 256, 2, 1, 1),
 };
 const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
