@@ -733,7 +733,9 @@ const CUtensorMap& tensor_map(Handle& h, int slab, const double* base, int narr,
     const long long plane = h.plane_elems();
     if (interior) {
         const double* b0 = base + (size_t)s.zout_lo * plane + (size_t)h.R * h.pitch + h.off + h.R;
-        e->map = make_map(b0, h.nx, h.ny, s.zout_hi - s.zout_lo, 1, h.pitch, plane, 0, bx, by);
+        // TMA stores clip x at 16-byte granularity: an odd nx's last column shares a granule
+        // with the x ghost, so the map stops at an even width and the kernel stores that column
+        e->map = make_map(b0, h.nx & ~1, h.ny, s.zout_hi - s.zout_lo, 1, h.pitch, plane, 0, bx, by);
     } else {
         e->map = make_map(base, h.pitch, h.Y, s.Zloc, narr, h.pitch, plane, plane * s.Zloc, bx, by);
     }

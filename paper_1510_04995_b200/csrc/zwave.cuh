@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(NT, MINB)
         const int ya0 = ug.ty * OY + R - H;
 
         // ghost columns (ghost value instead of the stencil) and in-allocation columns
-        uint32_t ghost_mask = 0, ok_mask = 0;
+        uint32_t ghost_mask = 0, ok_mask = 0, odd_mask = 0;
         int colidx[2 * PPT];  // row offset within a plane (allocated coordinates)
 #pragma unroll
         for (int i = 0; i < PPT; ++i)
@@ -412,11 +412,17 @@ __global__ void __launch_bounds__(NT, MINB)
                 const int xa = xa0 + (lcell[i] + q) % LX, ya = ya0 + lcell[i] / LX;
                 if (xa >= 0 && xa < p.X && ya >= 0 && ya < p.Y) ok_mask |= 1u << b;
                 if (xa < R || xa >= R + p.nx || ya < R || ya >= R + p.ny) ghost_mask |= 1u << b;
+                // TMA stores clip x at 16-byte granularity, so the store map stops at an even
+                // nx and an odd nx's last interior column is stored directly (odd_mask)
+                if ((p.nx & 1) && xa == R + p.nx - 1 && ya >= R && ya < R + p.ny &&
+                    ((out_mask >> b) & 1))
+                    odd_mask |= 1u << b;
                 const int cx = min(max(xa, 0), p.X - 1), cy = min(max(ya, 0), p.Y - 1);
                 colidx[b] = cy * p.pitch + p.off + cx;
             }
         const uint32_t col_fix = ghost_mask & ok_mask;
         const bool any_ghost_col = __syncthreads_or(col_fix != 0);
+        const bool any_odd_col = (p.nx & 1) && ug.tx == p.tiles_x - 1;  // owner of the last column
 
         for (int it = 0; it < n_it; ++it, ++g) {
             const int j = ug.za - H + it;  // level-0 plane of this iteration
@@ -438,6 +444,26 @@ __global__ void __launch_bounds__(NT, MINB)
                 }
                 issue_v();
                 issue_a();
+            }
+            // ghost values of the intermediate levels this iteration (boundary tiles and ghost
+            // planes only), loaded before the TMA waits so their latency overlaps them. Level TB
+            // needs none: the interior-only store map clips its ghost cells.
+            double2 gh[TB > 1 ? TB - 1 : 1][PPT];
+#pragma unroll
+            for (int s = 1; s < TB; ++s) {
+                const int k = j - s * R;
+                if (it < 2 * s * R || k < 0 || k >= p.Zloc) continue;
+                const int kg = k + p.zoff;
+                const bool plane_ghost = kg < R || kg >= R + p.nzg;
+                if (!(plane_ghost || any_ghost_col)) continue;
+                const double* ghost = p.ghost[(p.parity0 + s) & 1] + (long long)k * p.plane;
+                const uint32_t fix = plane_ghost ? ok_mask : col_fix;
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) {
+                    if (dyv[i] < s * R) continue;
+                    if ((fix >> (2 * i)) & 1) gh[s - 1][i].x = __ldg(ghost + colidx[2 * i]);
+                    if ((fix >> (2 * i + 1)) & 1) gh[s - 1][i].y = __ldg(ghost + colidx[2 * i + 1]);
+                }
             }
             mbar_wait(&vbar[g % NR0], (g / NR0) & 1);
             if constexpr (NAUX > 0) mbar_wait(&abar[g % NAR], (g / NAR) & 1);
@@ -587,14 +613,13 @@ __global__ void __launch_bounds__(NT, MINB)
                 }
                 // (2) ghost cells of level s hold the parity-(t0+s) field's ghosts (block edges
                 //     and ghost planes only: a uniform branch elsewhere)
-                if (plane_ghost || any_ghost_col) {
-                    const double* ghost = p.ghost[(p.parity0 + s) & 1] + (long long)k * p.plane;
+                if (s < TB && (plane_ghost || any_ghost_col)) {
                     const uint32_t fix = plane_ghost ? ok_mask : col_fix;
 #pragma unroll
                     for (int i = 0; i < PPT; ++i) {
                         if (dyv[i] < s * R) continue;
-                        if ((fix >> (2 * i)) & 1) val[i].x = __ldg(ghost + colidx[2 * i]);
-                        if ((fix >> (2 * i + 1)) & 1) val[i].y = __ldg(ghost + colidx[2 * i + 1]);
+                        if ((fix >> (2 * i)) & 1) val[i].x = gh[s < TB ? s - 1 : 0][i].x;
+                        if ((fix >> (2 * i + 1)) & 1) val[i].y = gh[s < TB ? s - 1 : 0][i].y;
                     }
                 }
                 // (3) results: the level-s centre ring + z queue input (s < TB) or the output
@@ -614,6 +639,14 @@ __global__ void __launch_bounds__(NT, MINB)
                     for (int i = 0; i < PPT; ++i) {
                         if ((out_mask >> (2 * i)) & 1) stg[sidx[i]] = val[i].x;  // clipped by omap
                         if ((out_mask >> (2 * i + 1)) & 1) stg[sidx[i] + 1] = val[i].y;
+                    }
+                    if (any_odd_col && k >= p.zout_lo && k < p.zout_hi) {
+                        double* dst = p.dst_final + (long long)k * p.plane;
+#pragma unroll
+                        for (int i = 0; i < PPT; ++i) {
+                            if ((odd_mask >> (2 * i)) & 1) dst[colidx[2 * i]] = val[i].x;
+                            if ((odd_mask >> (2 * i + 1)) & 1) dst[colidx[2 * i + 1]] = val[i].y;
+                        }
                     }
                     if (has_penult) {  // final pass only: level TB-1 of the same cells
                         double* pen = p.dst_penult + (long long)k * p.plane;
