@@ -83,7 +83,7 @@ struct KindInfo {
     int default_tb;
 };
 const KindInfo kKinds[4] = {
-    {"const7pt", 1, 2, 7, 1, 0, 16, 10, 2},
+    {"const7pt", 1, 2, 7, 1, 0, 16, 10, 1},
     {"var7pt", 1, 9, 13, 1, 7, 72, 13, 2},
     {"const25pt", 4, 3, 33, 2, 1, 32, 33, 1},
     {"var25pt", 4, 15, 37, 1, 13, 120, 37, 1},

@@ -8,12 +8,12 @@ const Variant kVariantsConst7[] = {
     GIRIH_VARIANT(K_CONST7, 1, 64, 16, 128, 4, 0, 3),
     GIRIH_VARIANT(K_CONST7, 1, 64, 8, 128, 4, 0, 6),
     GIRIH_VARIANT(K_CONST7, 1, 64, 32, 512, 6, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 2, 64, 16, 256, 3, 0, 2),
     GIRIH_VARIANT(K_CONST7, 2, 64, 32, 512, 4, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 3, 64, 32, 512, 3, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 2, 64, 16, 256, 3, 0, 2),
     GIRIH_VARIANT(K_CONST7, 3, 64, 32, 256, 3, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 4, 64, 32, 512, 2, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 3, 64, 32, 512, 3, 0, 1),
     GIRIH_VARIANT(K_CONST7, 4, 64, 32, 256, 2, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 4, 64, 32, 512, 2, 0, 1),
 };
 const int kNumVariantsConst7 = sizeof(kVariantsConst7) / sizeof(kVariantsConst7[0]);
 

@@ -246,7 +246,11 @@ struct ZwaveConfig {
     static constexpr int AXO = R & ~1, AYO = R;
     static constexpr int AX = LX - 2 * AXO, AY = LY - 2 * AYO;
     static constexpr int AYX = AX * AY;
-    static constexpr int NAR = NAUX > 0 ? (TB - 1) * R + 1 + PA : 0;  // aux ring depth
+    // var7pt with TB = 2 keeps each pair's coefficients in registers from level 1 to level 2
+    // (same cells, R iterations later), so only level 1 reads the aux ring (deeper TB would need
+    // 28 more registers per level and spills)
+    static constexpr bool CQ = KIND == K_VAR7 && TB == 2;
+    static constexpr int NAR = NAUX > 0 ? (CQ ? 1 : (TB - 1) * R + 1) + PA : 0;  // aux ring depth
     static constexpr int AUXPLANE = NAUX * AYX;
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
     static constexpr int GUARD = round16(LX * R + R + 8);
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(NT, MINB)
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
     constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA, OY = CFG::OY;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
+    constexpr bool CQ = CFG::CQ;
     constexpr int AX = CFG::AX, AYX = CFG::AYX, AUXPLANE = CFG::AUXPLANE;
     constexpr int GUARD = CFG::GUARD, STAGE = CFG::STAGE;
     constexpr uint32_t PLANE_BYTES = CELLS * sizeof(double);
@@ -381,7 +386,20 @@ __global__ void __launch_bounds__(NT, MINB)
         ai[i] = (ly - AYO) * AX + (lx - AXO);
         sidx[i] = (ly - H) * p.ox + (lx - p.hx);
     }
+    // pairs whose whole warp lies outside the level-s valid rows skip the stencil (warp-uniform;
+    // their values are never read): bit (s-1)*PPT + i. Only for R = 1: the 25-point bodies are
+    // long enough that the per-pair branch costs more interleaving than the skipped work saves.
+    static_assert(TB * PPT <= 32, "warp skip mask");
+    uint32_t wskip = 0;
+#pragma unroll
+    for (int s = 1; s <= (R == 1 ? TB : 0); ++s)
+#pragma unroll
+        for (int i = 0; i < PPT; ++i)
+            if (__all_sync(0xffffffffu, dyv[i] < s * R)) wskip |= 1u << ((s - 1) * PPT + i);
     const bool has_penult = p.dst_penult != nullptr;
+    // coefficient queue (CQ): cq[L][pair] = coefficients level 1 used L+1 iterations ago
+    constexpr int CQD = CQ ? TB - 1 : 1, CQN = CQ ? 7 : 1;
+    double2 cq[CQD][PPT][CQN], cnew[PPT][CQN];
     // per-thread z queues: zq[L][pair][d] = level L at plane (newest_L - 2R + d), d = 0..2R-1
     double2 zq[TB][PPT][2 * R];
 #pragma unroll
@@ -512,8 +530,12 @@ __global__ void __launch_bounds__(NT, MINB)
                 double2 val[PPT];
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
-                    // every pair computes (straight-line code the compiler can interleave);
-                    // rows outside the level-s valid area produce values no valid cell reads
+                    // every pair of a warp with a valid row computes (straight-line code the
+                    // compiler can interleave); invalid rows produce values no valid cell reads
+                    if ((wskip >> ((s - 1) * PPT + i)) & 1) {
+                        val[i] = make_double2(0.0, 0.0);
+                        continue;
+                    }
                     const int h2 = lcell[i] >> 1;  // pair index within a plane
                     // x neighbourhood x = c-XA .. c+1+XA from XA+1 aligned pair loads
                     double xs[2 * XA + 2];
@@ -548,8 +570,17 @@ __global__ void __launch_bounds__(NT, MINB)
                     } else if constexpr (KIND == K_VAR7) {
                         const double2 yp = Yp(1), ym = Yp(-1), zp = Zp(1), zm = Zp(-1);
                         double2 cf[7];
+                        if (!CQ || s == 1) {
 #pragma unroll
-                        for (int a = 0; a < 7; ++a) cf[a] = Cp(a);
+                            for (int a = 0; a < 7; ++a) cf[a] = Cp(a);
+                            if constexpr (CQ) {
+#pragma unroll
+                                for (int a = 0; a < 7; ++a) cnew[i][a] = cf[a];
+                            }
+                        } else {
+#pragma unroll
+                            for (int a = 0; a < 7; ++a) cf[a] = cq[CQ ? s - 2 : 0][i][CQ ? a : 0];
+                        }
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
                             double v = dmul(comp(cf[0], q), X(q, 0));
@@ -671,7 +702,19 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) wr[lcell[i] >> 1] = fresh[L][i];
             }
-            // advance every level's z queue by one plane
+            // advance every level's z queue by one plane (and the coefficient queue)
+            if constexpr (CQ) {
+#pragma unroll
+                for (int L = CQD - 1; L > 0; --L)
+#pragma unroll
+                    for (int i = 0; i < PPT; ++i)
+#pragma unroll
+                        for (int a = 0; a < CQN; ++a) cq[L][i][a] = cq[L - 1][i][a];
+#pragma unroll
+                for (int i = 0; i < PPT; ++i)
+#pragma unroll
+                    for (int a = 0; a < CQN; ++a) cq[0][i][a] = cnew[i][a];
+            }
 #pragma unroll
             for (int L = 0; L < TB; ++L) {
 #pragma unroll

@@ -10,7 +10,7 @@ def smem(kind, tb, lx, ly, nt, p, pa):
     OY = ly - 2 * H; OXM = lx - 2 * H; CELLS = lx * ly
     NRING = NR0 + (tb - 1) * QL
     NAUX = NAUXA[kind]; AXO = R & ~1; AX = lx - 2 * AXO; AY = ly - 2 * R
-    NAR = (tb - 1) * R + 1 + pa if NAUX else 0
+    NAR = ((1 if (kind == 1 and tb == 2) else (tb - 1) * R + 1) + pa) if NAUX else 0
     AUXPLANE = NAUX * AX * AY
     GUARD = r16(lx * R + R + 8); STAGE = r16(OXM * OY)
     d = 2 * GUARD + NRING * CELLS + NAR * AUXPLANE + 3 * STAGE
