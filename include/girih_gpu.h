@@ -152,6 +152,25 @@ int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_pass
                    int* n_passes, int* pass_tb, int* pass_src, int* pass_src_prev,
                    int* pass_dst, int* pass_dst_penult);
 
+/* GPU analogue of the analytic models (proj/src/models.cpp:12-84; cache_block_size, code_balance,
+ * roofline): tile geometry, shared-memory footprint per CTA (the counterpart of Eq. 2's C_S),
+ * redundant halo recompute, code balance (algorithmic B1/Tb and the no-L2-reuse bound) and the
+ * roofline min(HBM*Tb/B1, FP64/(DP ops*redundancy)) of one (kind, grid, tb, variant). tb = 0 /
+ * variant = -1 select the defaults; hbm_gbs / fp64_ops <= 0 select the measured B200 peaks
+ * (6558.7 GB/s copy, 18.59e12 DADD/DMUL ops/s). Host-only (no device needed). */
+typedef struct {
+    int tb, variant, lx, ly, ox, oy, threads;
+    int smem_bytes;          /* dynamic shared memory per CTA */
+    int ctas_per_sm;         /* resident CTAs per SM allowed by shared memory and threads */
+    int tiles_x, tiles_y, zchunks, zc_len;
+    double redundancy;       /* evaluated level-cell updates per useful LUP */
+    double code_balance;     /* algorithmic bytes/LUP, B1/Tb */
+    double code_balance_no_l2; /* bytes/LUP if every tile re-streamed its whole box from HBM */
+    double hbm_mlups, fp64_mlups, roofline_mlups;
+} girih_gpu_model_out;
+int girih_gpu_model(int kind, int nx, int ny, int nz, int tb, int variant, double hbm_gbs,
+                    double fp64_ops, girih_gpu_model_out* out);
+
 /* z-slab decomposition used by multi-GPU handles: slab g of nslabs owns interior planes
  * [*z0, *z1) (0-based interior z) and carries *hz halo planes per side (R * max fused depth). */
 int girih_gpu_slab_layout(int kind, int nz, int nslabs, int g, int* z0, int* z1, int* hz);

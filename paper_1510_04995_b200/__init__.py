@@ -6,7 +6,8 @@ is its host-side mirror of the reference's stencil/run interface.
 from ._lib import GirihError, InvalidArgument, LIB_PATH, load
 from .stencil import (CONST7PT, CONST25PT, KINDS, VAR7PT, VAR25PT, DeviceState, GpuConfig,
                       GridSpec, PerfReport, ProblemState, StencilTraits, device_info, fp64_peak,
-                      init_state, interior_checksum, nccl_unique_id, pinned_empty, plan, run,
+                      init_state, interior_checksum, model, nccl_unique_id, pinned_empty, plan,
+                      run,
                       slab_layout,
                       stencil_from_name,
                       traits, variants)
@@ -14,6 +15,6 @@ from .stencil import (CONST7PT, CONST25PT, KINDS, VAR7PT, VAR25PT, DeviceState, 
 __all__ = [
     "CONST7PT", "VAR7PT", "CONST25PT", "VAR25PT", "KINDS", "DeviceState", "GpuConfig", "GridSpec",
     "PerfReport", "ProblemState", "StencilTraits", "GirihError", "InvalidArgument", "LIB_PATH",
-    "device_info", "fp64_peak", "init_state", "interior_checksum", "load", "nccl_unique_id", "pinned_empty", "plan",
+    "device_info", "fp64_peak", "init_state", "interior_checksum", "load", "model", "nccl_unique_id", "pinned_empty", "plan",
     "run", "slab_layout", "stencil_from_name", "traits", "variants",
 ]

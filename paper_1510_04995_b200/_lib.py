@@ -61,6 +61,14 @@ class GirihGpuVariant(C.Structure):
 # every symbol include/girih_gpu.h declares, with (restype, argtypes)
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
+class GirihGpuModel(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("tb", "variant", "lx", "ly", "ox", "oy", "threads",
+                                        "smem_bytes", "ctas_per_sm", "tiles_x", "tiles_y",
+                                        "zchunks", "zc_len")] + \
+               [(n, C.c_double) for n in ("redundancy", "code_balance", "code_balance_no_l2",
+                                           "hbm_mlups", "fp64_mlups", "roofline_mlups")]
+
+
 SIGNATURES = {
     "girih_gpu_last_error": (C.c_char_p, []),
     "girih_gpu_abi_version": (C.c_int, []),
@@ -89,6 +97,8 @@ SIGNATURES = {
     "girih_gpu_plan": (C.c_int, [C.c_int, C.c_longlong, C.c_longlong, C.c_int, C.c_int,
                                  _ip, _ip, _ip, _ip, _ip, _ip]),
     "girih_gpu_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ip]),
+    "girih_gpu_model": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_double, C.c_double, C.POINTER(GirihGpuModel)]),
     "girih_gpu_tune": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(GirihGpuConfig), _dp, _ip]),
     "girih_gpu_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "girih_gpu_host_free": (C.c_int, [C.c_void_p]),

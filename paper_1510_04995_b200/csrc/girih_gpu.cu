@@ -804,14 +804,48 @@ int occupancy_of(const Variant* var) {
     return occ;
 }
 
+// Tile grid of one pass: x halo, output tile, tile counts, z chunks and the level-cell updates
+// it evaluates (shared by build_params and the analytic model girih_gpu_model).
+struct TileGeom {
+    int hx, ox, oy, tiles_x, tiles_y, nzc, zc_len, units;
+    long long computed_lups;
+};
+
+TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max_grid) {
+    TileGeom t{};
+    const int R = h.R, H = tb * R;
+    // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
+    t.hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
+    t.ox = var->lx - 2 * t.hx;
+    t.oy = var->ly - 2 * H;
+    t.tiles_x = (h.nx + t.ox - 1) / t.ox;
+    t.tiles_y = (h.ny + t.oy - 1) / t.oy;
+    const int txy = t.tiles_x * t.tiles_y;
+    t.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
+                              : choose_zchunks(nzl, H, h.nc, txy, max_grid);
+    t.zc_len = (nzl + t.nzc - 1) / t.nzc;
+    t.nzc = (nzl + t.zc_len - 1) / t.zc_len;
+    t.units = txy * t.nzc;
+    // level s covers (OX + 2(TB-s)R) x (OY + 2(TB-s)R) per tile column and
+    // nzl + 2 nzc (TB-s) R planes
+    t.computed_lups = 0;
+    for (int lev = 1; lev <= tb; ++lev) {
+        const long long ex = (long long)(t.ox + 2 * (t.hx - lev * R));
+        const long long ey = (long long)(t.oy + 2 * (tb - lev) * R);
+        const long long ez = (long long)nzl + 2LL * t.nzc * (tb - lev) * R;
+        t.computed_lups += ex * ey * (long long)txy * ez;
+    }
+    return t;
+}
+
 // Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
 PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_index,
                         long long t0, LaunchInfo* li) {
     Slab& s = h.slabs[slab_index];
-    const int R = h.R, H = ps.tb * R;
-    // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
-    const int hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
-    const int OX = var->lx - 2 * hx, OY = var->ly - 2 * H;
+    const int nzl = s.zout_hi - s.zout_lo;
+    const int max_grid = h.sm_count * occupancy_of(var);
+    const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid);
+    const int hx = tg.hx, OX = tg.ox;
     PassParams p{};
     p.hx = hx;
     p.ox = OX;
@@ -833,18 +867,13 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.Zloc = s.Zloc;
     p.zoff = s.zoff;
     p.nzg = h.nz;
-    p.tiles_x = (h.nx + OX - 1) / OX;
-    p.tiles_y = (h.ny + OY - 1) / OY;
+    p.tiles_x = tg.tiles_x;
+    p.tiles_y = tg.tiles_y;
     p.zout_lo = s.zout_lo;
     p.zout_hi = s.zout_hi;
-    const int nzl = s.zout_hi - s.zout_lo;
-    int occ = occupancy_of(var);
-    const int max_grid = h.sm_count * occ;
-    const int txy = p.tiles_x * p.tiles_y;
-    p.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl) : choose_zchunks(nzl, H, h.nc, txy, max_grid);
-    p.zc_len = (nzl + p.nzc - 1) / p.nzc;
-    p.nzc = (nzl + p.zc_len - 1) / p.zc_len;
-    p.units = txy * p.nzc;
+    p.nzc = tg.nzc;
+    p.zc_len = tg.zc_len;
+    p.units = tg.units;
     p.work = reinterpret_cast<int*>(s.work->p);
     p.trace = nullptr;
     if (std::getenv("GIRIH_TRACE")) {
@@ -854,15 +883,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     }
     li->grid = std::min(p.units, max_grid);
     li->zchunks = p.nzc;
-    // computed LUPs: level s covers (OX + 2(TB-s)R) x (OY + 2(TB-s)R) per tile column and
-    // nzl + 2 nzc (TB-s) R planes
-    li->computed_lups = 0;
-    for (int lev = 1; lev <= ps.tb; ++lev) {
-        const long long ex = (long long)(OX + 2 * (hx - lev * R));
-        const long long ey = (long long)(OY + 2 * (ps.tb - lev) * R);
-        const long long ez = (long long)nzl + 2LL * p.nzc * (ps.tb - lev) * R;
-        li->computed_lups += ex * ey * (long long)txy * ez;
-    }
+    li->computed_lups = tg.computed_lups;
     return p;
 }
 
@@ -1528,6 +1549,57 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         best->zchunks = zopts[bz];
         if (best_mlups) *best_mlups = bs;
         if (n_measured) *n_measured = measured;
+    });
+}
+
+int girih_gpu_model(int kind, int nx, int ny, int nz, int tb, int variant, double hbm_gbs,
+                    double fp64_ops, girih_gpu_model_out* out) {
+    return guarded([&] {
+        if (!out) throw_err(GIRIH_EINVAL, "null argument");
+        Handle h;
+        setup_geometry(h, kind, nx, ny, nz, 0);
+        const KindInfo& ki = kind_info(kind);
+        if (tb == 0) tb = ki.default_tb;
+        if (tb < 1 || tb > max_tb(kind)) throw_err(GIRIH_EINVAL, "fused step count out of range");
+        h.cfg = default_config();
+        h.cfg.tb = tb;
+        const Variant* var = select_variant(kind, tb, variant);
+        if (var->tb != tb) throw_err(GIRIH_EINVAL, "variant does not match the fused depth");
+        // resident CTAs per SM from shared memory (1 KB reserved per CTA) and threads; the
+        // register bound needs the device and is left to the occupancy query at run time
+        const int per_sm = std::max(1, std::min(233472 / (var->smem_bytes + 1024), 2048 / var->threads));
+        const int sms = 148;
+        const TileGeom tg = tile_geom(h, tb, var, nz, sms * per_sm);
+        const double useful = double(nx) * ny * nz;
+        std::memset(out, 0, sizeof *out);
+        out->tb = tb;
+        out->variant = global_index_of(var);
+        out->lx = var->lx;
+        out->ly = var->ly;
+        out->ox = tg.ox;
+        out->oy = tg.oy;
+        out->threads = var->threads;
+        out->smem_bytes = var->smem_bytes;
+        out->ctas_per_sm = per_sm;
+        out->tiles_x = tg.tiles_x;
+        out->tiles_y = tg.tiles_y;
+        out->zchunks = tg.nzc;
+        out->zc_len = tg.zc_len;
+        out->redundancy = double(tg.computed_lups) / (useful * tb);
+        out->code_balance = double(ki.b1) / tb;
+        // no L2 reuse: every unit streams its whole level-0 box and aux box over its z range
+        // (chunk + 2H planes) from HBM and writes its output tile once
+        const int H = tb * h.R;
+        const int naux = kind == K_CONST7 ? 0 : kind == K_CONST25 ? 2 : ki.ncoeff;
+        const double per_unit = 8.0 * (double(var->lx) * var->ly * (tg.zc_len + 2 * H) +
+                                       double(naux) * var->aux_x * var->aux_y * (tg.zc_len + 2 * H - 2 * h.R) +
+                                       double(tg.ox) * tg.oy * tg.zc_len);
+        out->code_balance_no_l2 = per_unit * tg.units / (useful * tb);
+        const double hbm = (hbm_gbs > 0 ? hbm_gbs : 6558.7) * 1e9;
+        const double fp = fp64_ops > 0 ? fp64_ops : 18.59e12;
+        out->hbm_mlups = hbm * tb / ki.b1 / 1e6;
+        out->fp64_mlups = fp / (ki.dp_ops * out->redundancy) / 1e6;
+        out->roofline_mlups = std::min(out->hbm_mlups, out->fp64_mlups);
     });
 }
 

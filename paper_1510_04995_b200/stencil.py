@@ -229,6 +229,18 @@ def slab_layout(kind: int, nz: int, nslabs: int, g: int):
     return z0.value, z1.value, hz.value
 
 
+def model(kind: int, grid: "GridSpec", tb: int = 0, variant: int = -1, hbm_gbs: float = 0.0,
+          fp64_ops: float = 0.0) -> dict:
+    """GPU analogue of the reference's analytic models (proj/src/models.cpp:12-84): tile geometry,
+    shared memory per CTA, redundancy, code balance and roofline of one configuration (host-only;
+    see girih_gpu_model in include/girih_gpu.h)."""
+    from ._lib import GirihGpuModel
+    out = GirihGpuModel()
+    check(load().girih_gpu_model(int(kind), grid.nx, grid.ny, grid.nz, int(tb), int(variant),
+                                 float(hbm_gbs), float(fp64_ops), C.byref(out)))
+    return {name: getattr(out, name) for name, _ in GirihGpuModel._fields_}
+
+
 def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     """A numpy array in page-locked host memory (freed when the array is collected)."""
     nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize

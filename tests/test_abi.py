@@ -123,3 +123,28 @@ def test_planner_rejects_bad_input(girih):
         girih.plan(0, 0, 5, 0)
     with pytest.raises(ValueError):
         girih.plan(9, 0, 5, 1)
+
+
+def test_model_matches_roofline_algebra(girih):
+    # girih_gpu_model: the GPU counterpart of models.cpp (code_balance / roofline); host-only
+    B1 = {0: 16, 1: 72, 2: 32, 3: 120}
+    DP = {0: 10, 1: 13, 2: 33, 3: 37}
+    grid = girih.GridSpec(512, 512, 512, 0)
+    for kind in range(4):
+        for tb in sorted({v["tb"] for v in girih.variants() if v["kind"] == kind}):
+            m = girih.model(kind, grid, tb, hbm_gbs=6000.0, fp64_ops=18e12)
+            assert m["tb"] == tb and m["code_balance"] == B1[kind] / tb
+            assert m["redundancy"] >= 1.0 and m["code_balance_no_l2"] > m["code_balance"]
+            assert m["hbm_mlups"] == pytest.approx(6000e9 * tb / B1[kind] / 1e6)
+            assert m["fp64_mlups"] == pytest.approx(18e12 / (DP[kind] * m["redundancy"]) / 1e6)
+            assert m["roofline_mlups"] == min(m["hbm_mlups"], m["fp64_mlups"])
+            assert m["tiles_x"] * m["ox"] >= 512 and m["tiles_y"] * m["oy"] >= 512
+            assert m["zchunks"] * m["zc_len"] >= 512 and m["ctas_per_sm"] >= 1
+            v = girih.variants()[m["variant"]]
+            assert (v["kind"], v["tb"], v["smem_bytes"]) == (kind, tb, m["smem_bytes"])
+        # Tb = 1 redundancy is the halo of one step only
+        assert girih.model(kind, grid, 1)["redundancy"] < 1.2
+    with pytest.raises(ValueError):
+        girih.model(0, grid, 99)
+    with pytest.raises(ValueError):
+        girih.model(0, girih.GridSpec(2, 2, 2, 0), 1)

@@ -69,3 +69,20 @@ def test_cli_run_record_and_tune_cache(tmp_path):
     assert r.returncode == 0 and r.stdout.startswith("cached")
     r = run("run", "--stencil", "var7pt", "--n", 48, "--nt", 4, "--use-tuned", tuned)
     assert r.returncode == 0, r.stderr
+
+
+@needs_cli
+def test_cli_model_prints_gpu_and_cpu_models():
+    # models.cpp analogue: one CSV line per (stencil, fused depth); host-only, no device
+    r = run("model", "--all", "--n", 512)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    hdr = lines[0].split(",")
+    rows = [dict(zip(hdr, l.split(","))) for l in lines[1:]]
+    assert {x["stencil"] for x in rows} == {"const7pt", "var7pt", "const25pt", "var25pt"}
+    for x in rows:
+        b1 = {"const7pt": 16, "var7pt": 72, "const25pt": 32, "var25pt": 120}[x["stencil"]]
+        assert abs(float(x["gpu_code_balance"]) * int(x["tb"]) - b1) < 0.01
+    # the reference's own Eq. 4 and spatial balance ride along (models.cpp:27-49)
+    v7 = [x for x in rows if x["stencil"] == "var7pt"][0]
+    assert float(v7["cpu_spatial_balance"]) == 80.0

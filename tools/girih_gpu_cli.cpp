@@ -10,6 +10,9 @@
 //                    [--out FILE] [--format csv|json] [--use-tuned FILE]   (main.cpp:260-328)
 //   girih_gpu tune   [--stencil S] [--nx ..] [--max-tb K] [--out FILE] [--force]
 //                                                                         (main.cpp:395-469)
+//   girih_gpu model  [--stencil S | --all] [--nx ..] [--tb K] [--variant V] [--hbm GBS]
+//                    [--fp64 OPS]   GPU analogue of the analytic models (models.cpp:12-84),
+//                    printed beside the reference's CPU code balance / spatial balance
 // Exit codes follow main.cpp:185, 524-527: 0 pass, 1 verification failure, 2 error.
 #include <cmath>
 #include <cstdio>
@@ -23,6 +26,7 @@
 #include <vector>
 
 #include "girih/engine.hpp"
+#include "girih/models.hpp"
 #include "girih/stencil.hpp"
 #include "girih_gpu.hpp"
 
@@ -40,6 +44,7 @@ struct Options {
     unsigned long long seed = 42;
     bool all = false, inject_fault = false, remap = false, force = false;
     int tb = 0, variant = -1, max_tb = 0;
+    double hbm = 0, fp64 = 0;
     std::string out, format = "csv", use_tuned;
 };
 
@@ -67,6 +72,8 @@ Options parse(int argc, char** argv) {
         else if (a == "--out") o.out = next();
         else if (a == "--format") o.format = next();
         else if (a == "--use-tuned") o.use_tuned = next();
+        else if (a == "--hbm") o.hbm = std::stod(next());
+        else if (a == "--fp64") o.fp64 = std::stod(next());
         else if (a == "--all") o.all = true;
         else if (a == "--inject-fault") o.inject_fault = true;
         else if (a == "--remap") o.remap = true;
@@ -327,6 +334,33 @@ int cmd_tune(const Options& o) {
     return 0;
 }
 
+// GPU model per fused depth next to the reference's CPU models (code_balance Eq. 4 at the
+// default diamond width, spatial_balance), one line per (stencil, tb)
+int cmd_model(const Options& o) {
+    std::vector<std::string> names = {o.stencil};
+    if (o.all) names = {"const7pt", "var7pt", "const25pt", "var25pt"};
+    std::cout << "stencil,tb,variant,tile,out_tile,threads,smem_bytes,ctas_per_sm,zchunks,"
+                 "redundancy,gpu_code_balance,gpu_code_balance_no_l2,hbm_mlups,fp64_mlups,"
+                 "roofline_mlups,cpu_code_balance_dw,cpu_spatial_balance\n";
+    for (const auto& name : names) {
+        const StencilKind kind = stencil_from_name(name);
+        const StencilTraits tr = traits(kind);
+        const int dw = tr.radius == 1 ? 8 : 16;  // main.cpp:67 defaults
+        std::vector<int> tbs = o.tb > 0 ? std::vector<int>{o.tb} : tbs_for(int(kind));
+        for (int tb : tbs) {
+            girih_gpu_model_out m{};
+            gpu::check(girih_gpu_model(int(kind), o.nx, o.ny, o.nz, tb, o.tb > 0 ? o.variant : -1,
+                                       o.hbm, o.fp64, &m));
+            std::printf("%s,%d,%d,%dx%d,%dx%d,%d,%d,%d,%d,%.4f,%.3f,%.3f,%.0f,%.0f,%.0f,%.3f,%.1f\n",
+                        name.c_str(), m.tb, m.variant, m.lx, m.ly, m.ox, m.oy, m.threads,
+                        m.smem_bytes, m.ctas_per_sm, m.zchunks, m.redundancy, m.code_balance,
+                        m.code_balance_no_l2, m.hbm_mlups, m.fp64_mlups, m.roofline_mlups,
+                        code_balance(dw, tr.domain_streams, tr.radius), spatial_balance(kind));
+        }
+    }
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -335,6 +369,7 @@ int main(int argc, char** argv) {
         if (o.cmd == "verify") return cmd_verify(o);
         if (o.cmd == "run") return cmd_run(o);
         if (o.cmd == "tune") return cmd_tune(o);
+        if (o.cmd == "model") return cmd_model(o);
         throw std::invalid_argument("unknown subcommand " + o.cmd);
     } catch (const std::exception& e) {
         std::cerr << "error: " << e.what() << '\n';
