@@ -134,6 +134,14 @@ int girih_gpu_step(void* handle, long long steps, girih_gpu_report* report);
 /* Download u, v and t_current into the view (u/v may be NULL to skip). */
 int girih_gpu_download(void* handle, girih_state_view* state);
 
+/* Device-side bitwise compare: field 0 = u, 1 = v, 2 + c = coefficient c
+ * of the device state against a host array in state-view layout (X*Y*Z doubles), streamed to the
+ * device in z blocks so a large state is checked without downloading it. *n_diff = number of
+ * differing cells (ghosts and pad included), *first_index = lowest differing linear index
+ * ((k*Y + j)*X + i) or -1. Each slab compares the planes it is authoritative for. */
+int girih_gpu_compare(void* handle, int field, const double* host, long long* n_diff,
+                      long long* first_index);
+
 /* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
 int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double* cc);
 

@@ -97,6 +97,8 @@ SIGNATURES = {
     "girih_gpu_plan": (C.c_int, [C.c_int, C.c_longlong, C.c_longlong, C.c_int, C.c_int,
                                  _ip, _ip, _ip, _ip, _ip, _ip]),
     "girih_gpu_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ip]),
+    "girih_gpu_compare": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_longlong)]),
     "girih_gpu_model": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_double, C.c_double, C.POINTER(GirihGpuModel)]),
     "girih_gpu_tune": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(GirihGpuConfig), _dp, _ip]),

@@ -10,6 +10,12 @@ cudaError_t launch_init_field(double* buf, int pitch, int off, int X, int Y, int
                               int Zg, uint64_t seed, int field, int remap, double scale,
                               cudaStream_t stream);
 
+// bitwise compare of local planes [k0, k0+nk) of a device-layout field with an X-pitched block
+cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, int Y, int k0,
+                                 int nk, const double* blk, long long base,
+                                 unsigned long long* count, unsigned long long* first,
+                                 int sm_count, cudaStream_t stream);
+
 // mode 0: separate DMUL+DADD chains (2 ops per step), mode 1: DFMA chains (2 flops per step)
 cudaError_t launch_fp64_probe(int mode, double* out, int blocks, int threads, int iters,
                               cudaStream_t stream);

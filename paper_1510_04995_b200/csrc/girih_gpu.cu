@@ -644,19 +644,25 @@ void copy_h2d(Handle& h, double* const dev_of_slab[], const double* host) {
     }
 }
 
+// global allocated planes [k0, k1) a slab is authoritative for (its own interior planes plus
+// the global ghost planes at the outer slabs)
+void auth_planes(const Handle& h, const Slab& s, int* k0, int* k1) {
+    if (s.gcount == 1) {
+        *k0 = 0;
+        *k1 = h.Z;
+    } else {
+        *k0 = s.zout_lo + s.zoff;
+        *k1 = s.zout_hi + s.zoff;
+        if (s.gidx == 0) *k0 = 0;               // lower ghost planes
+        if (s.gidx + 1 == s.gcount) *k1 = h.Z;  // upper ghost planes
+    }
+}
+
 void copy_d2h(Handle& h, double* const dev_of_slab[], double* host) {
     for (size_t g = 0; g < h.slabs.size(); ++g) {
         Slab& s = h.slabs[g];
-        int k0, k1;  // global planes this slab is authoritative for
-        if (s.gcount == 1) {
-            k0 = 0;
-            k1 = h.Z;
-        } else {
-            k0 = s.zout_lo + s.zoff;
-            k1 = s.zout_hi + s.zoff;
-            if (s.gidx == 0) k0 = 0;                     // lower ghost planes
-            if (s.gidx + 1 == s.gcount) k1 = h.Z;        // upper ghost planes
-        }
+        int k0, k1;
+        auth_planes(h, s, &k0, &k1);
         GCHECK(cudaSetDevice(s.device));
         double* dst = host + (size_t)k0 * h.Y * h.X;
         const double* src = dev_of_slab[g] + (size_t)(k0 - s.zoff) * h.plane_elems() + h.off;
@@ -1336,6 +1342,49 @@ int girih_gpu_download(void* handle, girih_state_view* state) {
         sync_all(h);
         state->t_current = h.t_current;
         std::memcpy(state->cc, h.cc, sizeof h.cc);
+    });
+}
+
+int girih_gpu_compare(void* handle, int field, const double* host, long long* n_diff,
+                      long long* first_index) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!host || !n_diff) throw_err(GIRIH_EINVAL, "null argument");
+        if (field < 0 || field >= 2 + h.nc) throw_err(GIRIH_EINVAL, "no such field");
+        const size_t plane_host = size_t(h.X) * h.Y;
+        // z blocks of <= 256 MB streamed through a device staging buffer
+        const int bk = int(std::max<size_t>(1, (size_t(256) << 20) / (plane_host * 8)));
+        unsigned long long total = 0, first = ~0ull;
+        for (Slab& s : h.slabs) {
+            int k0, k1;
+            auth_planes(h, s, &k0, &k1);
+            if (k1 <= k0) continue;
+            GCHECK(cudaSetDevice(s.device));
+            const double* dev = field < 2 ? s.buf[field]->p : s.coeff(field - 2, h.slab_elems(s));
+            DevBuf blk, ctr;
+            blk.device = ctr.device = s.device;
+            GCHECK(cudaMalloc(&blk.p, size_t(std::min(bk, k1 - k0)) * plane_host * 8));
+            GCHECK(cudaMalloc(&ctr.p, 16));
+            auto* cnt = reinterpret_cast<unsigned long long*>(ctr.p);
+            const unsigned long long init[2] = {0ull, ~0ull};
+            GCHECK(cudaMemcpyAsync(cnt, init, 16, cudaMemcpyHostToDevice, s.stream));
+            for (int kb = k0; kb < k1; kb += bk) {
+                const int nk = std::min(bk, k1 - kb);
+                GCHECK(cudaMemcpyAsync(blk.p, host + size_t(kb) * plane_host,
+                                       size_t(nk) * plane_host * 8, cudaMemcpyHostToDevice,
+                                       s.stream));
+                GCHECK(launch_compare_field(dev, h.pitch, h.off, h.X, h.Y, kb - s.zoff, nk, blk.p,
+                                            (long long)kb * (long long)plane_host, cnt, cnt + 1,
+                                            h.sm_count, s.stream));
+            }
+            unsigned long long res[2];
+            GCHECK(cudaMemcpyAsync(res, cnt, 16, cudaMemcpyDeviceToHost, s.stream));
+            GCHECK(cudaStreamSynchronize(s.stream));
+            total += res[0];
+            first = std::min(first, res[1]);
+        }
+        *n_diff = (long long)total;
+        if (first_index) *first_index = total ? (long long)first : -1;
     });
 }
 

@@ -52,6 +52,42 @@ cudaError_t launch_init_field(double* buf, int pitch, int off, int X, int Y, int
     return cudaGetLastError();
 }
 
+// ---- device-side bitwise compare of a device-layout field against an X-pitched host block ----
+// Local planes [k0, k0 + nk) of `dev` against `blk` ([nk][Y][X]); counts differing cells and
+// keeps the lowest global linear index (base + block index) of a difference.
+__global__ void compare_field_kernel(const double* __restrict__ dev, int pitch, int off, int X,
+                                     int Y, int k0, int nk, const double* __restrict__ blk,
+                                     long long base, unsigned long long* count,
+                                     unsigned long long* first) {
+    const long long n = static_cast<long long>(nk) * Y * X;
+    unsigned long long local = 0, lo = ~0ull;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(q % X);
+        const long long r = q / X;
+        const int j = static_cast<int>(r % Y);
+        const int k = static_cast<int>(r / Y);
+        const double a = dev[(static_cast<long long>(k0 + k) * Y + j) * pitch + off + i];
+        if (__double_as_longlong(a) != __double_as_longlong(blk[q])) {
+            ++local;
+            lo = min(lo, static_cast<unsigned long long>(base + q));
+        }
+    }
+    if (local) {
+        atomicAdd(count, local);
+        atomicMin(first, lo);
+    }
+}
+
+cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, int Y, int k0,
+                                 int nk, const double* blk, long long base,
+                                 unsigned long long* count, unsigned long long* first,
+                                 int sm_count, cudaStream_t stream) {
+    compare_field_kernel<<<sm_count * 8, 256, 0, stream>>>(dev, pitch, off, X, Y, k0, nk, blk,
+                                                           base, count, first);
+    return cudaGetLastError();
+}
+
 // ---- FP64 rate probe: independent chains of DADD/DMUL (bitwise mode) or DFMA ----
 template <int MODE>
 __global__ void fp64_probe_kernel(double* out, int iters, double a, double b) {

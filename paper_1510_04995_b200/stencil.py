@@ -339,6 +339,20 @@ class DeviceState:
             check(load().girih_gpu_download_coeffs(self._handle(), ptrs, len(state.coeffs), None))
         return state
 
+    def compare(self, field, host: np.ndarray):
+        """Bitwise compare of a device field ('u', 'v' or coefficient index c) with a host array
+        of the full allocated grid, on the device (girih_gpu_compare). Returns (n_diff, first)
+        with first = (i, j, k) of the lowest differing cell or None."""
+        f = {"u": 0, "v": 1}[field] if isinstance(field, str) else 2 + int(field)
+        arr = np.ascontiguousarray(host, dtype=np.float64)
+        n, first = C.c_longlong(), C.c_longlong()
+        check(load().girih_gpu_compare(self._handle(), f, _dptr(arr), C.byref(n), C.byref(first)))
+        if n.value == 0:
+            return 0, None
+        k, rem = divmod(first.value, arr.shape[1] * arr.shape[2])
+        j, i = divmod(rem, arr.shape[2])
+        return n.value, (i, j, k)
+
     def upload(self, state: ProblemState) -> None:
         v = _View(state)
         check(load().girih_gpu_upload(self._handle(), C.byref(v.view)))

@@ -244,3 +244,27 @@ def test_config1_full_size_bitwise(girih, oracle):
     oracle.naive_sweep(hs, 100)
     assert g.interior_checksum(st) == 0x9F26250C918339D4
     assert_state_equal(st, hs, "C1")
+
+
+@pytest.mark.parametrize("emulate", [0, 3])
+def test_device_side_compare(girih, oracle, emulate):
+    # the state is checked against the oracle ON the device (host blocks
+    # streamed in), including ghosts and pad, also across (emulated) z-slabs
+    g = girih
+    kind = 1
+    base = oracle.init_state(kind, 40, 33, 29, 2, 3, remap=True)
+    ref = base.copy()
+    oracle.naive_sweep(ref, 5)
+    cfg = g.GpuConfig(tb=2, emulate_slabs=emulate)
+    with g.DeviceState.from_state(to_problem(g, base), cfg) as ds:
+        ds.step(5)
+        assert ds.compare("u", ref.u) == (0, None)
+        assert ds.compare("v", ref.v) == (0, None)
+        for c in range(7):
+            assert ds.compare(c, base.coeffs[c]) == (0, None)
+        bad = ref.v.copy()
+        bad[7, 5, 3] += 1.0           # interior cell
+        bad[20, 0, 10] = -bad[20, 0, 10]  # y ghost
+        bad[28, 4, 41] = 7.0          # pad column
+        assert ds.compare("v", bad) == (3, (3, 5, 7))
+        assert ds.compare("u", ref.v)[0] > 0
