@@ -5,10 +5,11 @@
 namespace girih_gpu {
 
 const Variant kVariantsConst25[] = {
+    GIRIH_VARIANT(K_CONST25, 1, 64, 40, 256, 1, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 384, 1, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 256, 1, 1, 1),
     GIRIH_VARIANT(K_CONST25, 1, 64, 16, 128, 1, 1, 2),
-    GIRIH_VARIANT(K_CONST25, 1, 64, 32, 512, 1, 1, 1),
-    GIRIH_VARIANT(K_CONST25, 1, 64, 24, 384, 1, 1, 1),
-    GIRIH_VARIANT(K_CONST25, 2, 32, 32, 256, 2, 1, 1),
+    GIRIH_VARIANT(K_CONST25, 2, 32, 32, 192, 2, 1, 1),
 };
 const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
 

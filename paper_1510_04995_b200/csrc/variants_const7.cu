@@ -5,15 +5,13 @@
 namespace girih_gpu {
 
 const Variant kVariantsConst7[] = {
-    GIRIH_VARIANT(K_CONST7, 1, 64, 16, 128, 4, 0, 3),
-    GIRIH_VARIANT(K_CONST7, 1, 64, 8, 128, 4, 0, 6),
-    GIRIH_VARIANT(K_CONST7, 1, 64, 32, 512, 6, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 2, 64, 32, 512, 4, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 2, 64, 16, 256, 3, 0, 2),
-    GIRIH_VARIANT(K_CONST7, 3, 64, 32, 256, 3, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 3, 64, 32, 512, 3, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 4, 64, 32, 256, 2, 0, 1),
-    GIRIH_VARIANT(K_CONST7, 4, 64, 32, 512, 2, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 1, 64, 10, 128, 4, 0, 5),
+    GIRIH_VARIANT(K_CONST7, 1, 64, 18, 256, 4, 0, 2),
+    GIRIH_VARIANT(K_CONST7, 1, 64, 34, 512, 6, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 2, 64, 18, 256, 3, 0, 2),
+    GIRIH_VARIANT(K_CONST7, 2, 64, 34, 512, 4, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 3, 64, 32, 480, 3, 0, 1),
+    GIRIH_VARIANT(K_CONST7, 4, 64, 32, 480, 2, 0, 1),
 };
 const int kNumVariantsConst7 = sizeof(kVariantsConst7) / sizeof(kVariantsConst7[0]);
 

@@ -5,16 +5,17 @@
 namespace girih_gpu {
 
 const Variant kVariantsVar7[] = {
-    GIRIH_VARIANT(K_VAR7, 1, 64, 8, 128, 3, 1, 3),
     GIRIH_VARIANT(K_VAR7, 1, 64, 8, 64, 3, 1, 3),
-    GIRIH_VARIANT(K_VAR7, 1, 64, 16, 256, 4, 1, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 512, 2, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 512, 3, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 256, 2, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 32, 32, 512, 2, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 32, 16, 256, 2, 2, 2),
-    GIRIH_VARIANT(K_VAR7, 3, 32, 16, 256, 3, 1, 1),
-    GIRIH_VARIANT(K_VAR7, 4, 32, 16, 256, 2, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 8, 96, 3, 1, 3),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 10, 128, 3, 1, 2),
+    GIRIH_VARIANT(K_VAR7, 1, 64, 16, 224, 4, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 2, 2, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 3, 2, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 64, 16, 224, 2, 2, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 32, 32, 480, 2, 2, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 32, 16, 224, 2, 2, 2),
+    GIRIH_VARIANT(K_VAR7, 3, 32, 16, 224, 3, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 4, 32, 16, 224, 2, 1, 1),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

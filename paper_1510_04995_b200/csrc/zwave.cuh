@@ -238,7 +238,10 @@ struct ZwaveConfig {
     static constexpr int OY = LY - 2 * H;   // output tile height (x: runtime, halo H or H+1)
     static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
-    static constexpr int PPT = CELLS / (2 * NT);  // x-pairs of cells per thread
+    // threads cover the level-1 valid rows [R, LY - R) only: the R outermost rows of the
+    // loaded box are neighbours, never computed (for TB = 1 that is exactly the output rows)
+    static constexpr int CR = LY - 2 * R;
+    static constexpr int PPT = CR * LX / (2 * NT);  // x-pairs of cells per thread
     static constexpr int XA = 2 * ((R + 1) / 2);  // pair-aligned x reach (R=1: 2, R=4: 4)
     static constexpr int NRING = NR0 + (TB - 1) * QL;
     // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
@@ -258,7 +261,8 @@ struct ZwaveConfig {
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
                                            size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
-    static_assert(CELLS % (2 * NT) == 0, "tile must split evenly into cell pairs over the CTA");
+    static_assert((CR * LX) % (2 * NT) == 0, "computed rows must split evenly into cell pairs");
+    static_assert(NT % 32 == 0, "whole warps");
     static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
     static_assert(LX - 2 * H - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(NT, MINB)
     uint32_t out_mask = 0;
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
-        const int c = 2 * (tid + NT * i);  // first cell of the pair (even)
+        const int c = 2 * (tid + NT * i) + R * LX;  // first cell of the pair (even)
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
         const int dy = min(ly, LY - 1 - ly);

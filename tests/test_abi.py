@@ -47,8 +47,9 @@ def test_variants_registry(girih):
     assert {v["kind"] for v in vs} == {0, 1, 2, 3}
     for v in vs:
         assert v["smem_bytes"] <= 227 * 1024
-        assert v["lx"] * v["ly"] % v["threads"] == 0
         R = 1 if v["kind"] < 2 else 4
+        # threads cover the level-1 rows [R, ly - R) in x-pairs
+        assert v["lx"] * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
         assert v["lx"] > 2 * R * v["tb"] and v["ly"] > 2 * R * v["tb"]
     # every kind has a single-step variant and R=1 kinds fuse at least 4 steps
     for k in range(4):
