@@ -268,3 +268,19 @@ def test_device_side_compare(girih, oracle, emulate):
         bad[28, 4, 41] = 7.0          # pad column
         assert ds.compare("v", bad) == (3, (3, 5, 7))
         assert ds.compare("u", ref.v)[0] > 0
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_multi_tile_odd_extents(girih, oracle, kind):
+    # several tiles in x and y (tile x-seams, the odd-nx last column stored outside the TMA map,
+    # y-seams), with and without emulated slabs, every compiled TB
+    g = girih
+    base = oracle.init_state(kind, 131, 45, 37, 1, 21, remap=True)
+    for tb in tbs_for(g, kind):
+        steps = tb + 2
+        ref = base.copy()
+        oracle.naive_sweep(ref, steps)
+        for nslab in (0, 2):
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb, emulate_slabs=nslab))
+            assert_state_equal(st, ref, f"tb={tb} slabs={nslab}")
