@@ -1016,6 +1016,14 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     const long long t_begin = h.t_current;
     long long t = h.t_current;
     int pi = 0;
+    // one zeroed work counter per slab for the whole pass sequence: pass p draws units with
+    // atomicAdd - work_base (the sum of the earlier passes' unit counts; every pass performs
+    // exactly `units` increments), so no memset node separates consecutive passes
+    std::vector<long long> work_base(h.slabs.size(), 0);
+    for (Slab& s : h.slabs) {
+        GCHECK(cudaSetDevice(s.device));
+        GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+    }
     for (const Pass& ps : plan) {
         const Variant* var =
             select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
@@ -1026,7 +1034,9 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             Slab& s = h.slabs[g];
             GCHECK(cudaSetDevice(s.device));
             LaunchInfo li;
-            const PassParams p = build_params(h, ps, var, int(g), t, &li);
+            PassParams p = build_params(h, ps, var, int(g), t, &li);
+            p.work_base = int(work_base[g]);
+            work_base[g] += p.units;
             const CUtensorMap& vmap = tensor_map(h, int(g), s.buf[ps.src]->p, 1, var->lx, var->ly);
             const CUtensorMap* cmap = &vmap;
             const CUtensorMap* umap = &vmap;
@@ -1037,7 +1047,6 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 umap = &tensor_map(h, int(g), s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
             const CUtensorMap& omap = tensor_map(h, int(g), s.buf[ps.dst]->p, 1, p.ox,
                                                  var->ly - 2 * ps.tb * h.R, 1);
-            GCHECK(cudaMemsetAsync(p.work, 0, sizeof(int), s.stream));
             // inside a stream capture a plain record only orders streams: record as graph nodes
             const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
             if (time_passes && g == 0)

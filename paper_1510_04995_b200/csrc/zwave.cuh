@@ -66,6 +66,7 @@ struct PassParams {
     int tiles_x, tiles_y;    // tile grid
     int nzc, zc_len;         // z chunks per tile column and output planes per chunk
     int zout_lo, zout_hi;    // local output planes [lo, hi)
+    int work_base;           // value of *work when this pass started (cumulative per step)
     int units;               // tiles_x * tiles_y * nzc
     int* work;               // dynamic unit counter (zeroed before every launch)
     unsigned long long* trace;  // optional per-iteration phase clocks of CTA 0 (debug)
@@ -209,7 +210,7 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, vola
             // latency hides behind a whole unit instead of stalling the producer warp
             next = *drawn;
             if (next < p.units) {
-                const int d = int(gridDim.x) + atomicAdd(p.work, 1);
+                const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
                 *drawn = d < p.units ? d : p.units;
             }
             uq[(c.seq + 1) % UQ] = next;
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(NT, MINB)
         const int u0 = blockIdx.x < p.units ? int(blockIdx.x) : p.units;
         uq[0] = u0;
         if (u0 < p.units) {
-            const int d = int(gridDim.x) + atomicAdd(p.work, 1);
+            const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
             drawn = d < p.units ? d : p.units;
         } else {
             drawn = p.units;
