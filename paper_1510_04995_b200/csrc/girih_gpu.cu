@@ -793,11 +793,14 @@ int choose_zchunks(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
     // coefficient-heavy kinds: each chunk boundary re-streams (TB-1)R coefficient planes that
     // no longer sit in L2 (16.8 MB per 512^2 plane for var7pt), so their chunks are longer
     int len = ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
-    // small grids: shorten chunks until there are >= 2 units per resident CTA (latency-bound
-    // otherwise: few CTAs, each waiting on its own TMA pipeline)
+    // small grids: shorten chunks (in ~20% steps) until there are enough units per resident
+    // CTA that the last unit's tail is short against the pass: 5 for the light kinds
+    // (const7pt 256^3 +3%, const25pt 256^3 +10% over 2), 2 for the coefficient-heavy ones,
+    // whose re-streamed z halo costs more than the tail (var7pt 128^3: -7% at 5)
     const int min_len = std::max(4, 2 * H);
-    while (len > min_len && (long long)tiles_xy * ((nzl + len - 1) / len) < 2LL * grid)
-        len = std::max(min_len, len / 2);
+    const long long per_cta = ncoeff >= 7 ? 2 : 5;
+    while (len > min_len && (long long)tiles_xy * ((nzl + len - 1) / len) < per_cta * grid)
+        len = std::max(min_len, len * 4 / 5);
     return std::max(1, (nzl + len - 1) / len);
 }
 
