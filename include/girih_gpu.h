@@ -85,7 +85,8 @@ typedef struct {
     int variant_used;
     int zchunks_used;
     int grid_ctas;
-    int reserved;
+    int streamed;           /* girih_gpu_run: 1 = uploads, passes and downloads pipelined along z
+                               (skewed task graph; kernel_s is then the whole device span) */
 } girih_gpu_report;
 
 /* kernel variant description (compiled tile shapes) */
@@ -188,6 +189,10 @@ int girih_gpu_slab_layout(int kind, int nz, int nslabs, int g, int* z0, int* z1,
  * own state (the state is restored afterwards). Writes the best config into *best. */
 int girih_gpu_tune(void* handle, int max_tb, girih_gpu_config* best, double* best_mlups,
                    int* n_measured);
+
+/* Release the device memory the library keeps cached between handles (freed state buffers are
+ * reused by the next open/run of the same size instead of cudaMalloc/cudaFree per call). */
+int girih_gpu_trim(void);
 
 /* pinned host memory helpers (for H2D/D2H at full PCIe rate) */
 int girih_gpu_host_alloc(size_t bytes, void** ptr);

@@ -49,7 +49,7 @@ class GirihGpuReport(C.Structure):
         ("pass_s", C.c_double), ("computed_lups", C.c_longlong),
         ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong),
         ("variant_used", C.c_int), ("zchunks_used", C.c_int), ("grid_ctas", C.c_int),
-        ("reserved", C.c_int),
+        ("streamed", C.c_int),
     ]
 
 
@@ -99,6 +99,7 @@ SIGNATURES = {
     "girih_gpu_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ip]),
     "girih_gpu_compare": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(C.c_longlong),
                                     C.POINTER(C.c_longlong)]),
+    "girih_gpu_trim": (C.c_int, []),
     "girih_gpu_model": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_double, C.c_double, C.POINTER(GirihGpuModel)]),
     "girih_gpu_tune": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(GirihGpuConfig), _dp, _ip]),

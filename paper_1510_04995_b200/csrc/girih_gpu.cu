@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -352,18 +353,82 @@ CUtensorMap make_map(const double* base, long long dx, long long dy, long long d
 // ------------------------------------------------------------------------------------------
 // device state
 // ------------------------------------------------------------------------------------------
+// Device memory cache. girih_gpu_run opens and closes a handle per call; cudaMalloc + cudaFree
+// of the ~13 GB a var7pt 512^3 state needs cost 5 ms to 0.5 s per call (measured, erratic), so
+// freed blocks are kept per (device, size) and handed out again. Owners release blocks only
+// after the streams using them are synchronised. The cache holds at most kCap bytes, is flushed
+// and the allocation retried when cudaMalloc fails, and girih_gpu_trim() empties it.
+struct MemCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void*> blocks;
+    size_t bytes = 0;
+    static constexpr size_t kCap = size_t(64) << 30;
+};
+MemCache& mem_cache() {
+    static MemCache* c = new MemCache;  // never destroyed: no cudaFree after context teardown
+    return *c;
+}
+void mem_cache_flush(int device) {
+    MemCache& c = mem_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto it = c.blocks.begin(); it != c.blocks.end();) {
+        if (device >= 0 && it->first.first != device) {
+            ++it;
+            continue;
+        }
+        cudaSetDevice(it->first.first);
+        cudaFree(it->second);
+        c.bytes -= it->first.second;
+        it = c.blocks.erase(it);
+    }
+}
+cudaError_t dev_alloc(int device, size_t bytes, void** out) {
+    {
+        MemCache& c = mem_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.blocks.find({device, bytes});
+        if (it != c.blocks.end()) {
+            *out = it->second;
+            c.bytes -= bytes;
+            c.blocks.erase(it);
+            return cudaSuccess;
+        }
+    }
+    cudaSetDevice(device);
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        mem_cache_flush(device);
+        cudaSetDevice(device);
+        e = cudaMalloc(out, bytes);
+    }
+    return e;
+}
+void dev_free(int device, void* p, size_t bytes) {
+    if (!p) return;
+    MemCache& c = mem_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (bytes >= (size_t(1) << 20) && c.bytes + bytes <= MemCache::kCap) {
+            c.blocks.insert({{device, bytes}, p});
+            c.bytes += bytes;
+            return;
+        }
+    }
+    cudaSetDevice(device);
+    cudaFree(p);
+}
+
 struct DevBuf {
     double* p = nullptr;
     int device = 0;
+    size_t bytes = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() {
-        if (p) {
-            cudaSetDevice(device);
-            cudaFree(p);
-        }
-    }
+    ~DevBuf() { dev_free(device, p, bytes); }
+    // allocate `n` bytes on `dev` through the cache (throws on failure)
+    void alloc(int dev, size_t n);
 };
 
 struct StepStats {
@@ -472,12 +537,19 @@ NcclApi& nccl() {
             throw_err(GIRIH_ENCCL, std::string(#expr) + ": " + nccl().errorString(r_)); \
     } while (0)
 
+void DevBuf::alloc(int dev, size_t n) {
+    device = dev;
+    void* q = nullptr;
+    GCHECK(dev_alloc(dev, n, &q));
+    p = static_cast<double*>(q);
+    bytes = n;
+}
+
 void alloc_buf(std::unique_ptr<DevBuf>& b, int device, size_t elems, cudaStream_t st) {
     if (b) return;
     b = std::make_unique<DevBuf>();
-    b->device = device;
+    b->alloc(device, elems * sizeof(double));
     GCHECK(cudaSetDevice(device));
-    GCHECK(cudaMalloc(&b->p, elems * sizeof(double)));
     GCHECK(cudaMemsetAsync(b->p, 0, elems * sizeof(double), st));
 }
 
@@ -617,13 +689,16 @@ double* host_stage(Handle& h, Slab& s) {
     if (s.hstage_failed) return nullptr;
     s.hstage = std::make_unique<DevBuf>();
     s.hstage->device = s.device;
-    if (cudaMalloc(&s.hstage->p, size_t(h.X) * h.Y * s.Zloc * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();  // clear the sticky-free allocation error
-        s.hstage->p = nullptr;
+    void* q = nullptr;
+    const size_t n = size_t(h.X) * h.Y * s.Zloc * sizeof(double);
+    if (dev_alloc(s.device, n, &q) != cudaSuccess) {
+        cudaGetLastError();  // clear the (non-sticky) allocation error
         s.hstage.reset();
         s.hstage_failed = true;
         return nullptr;
     }
+    s.hstage->p = static_cast<double*>(q);
+    s.hstage->bytes = n;
     return s.hstage->p;
 }
 
@@ -857,9 +932,13 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
 
 // Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
 PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_index,
-                        long long t0, LaunchInfo* li) {
+                        long long t0, LaunchInfo* li, int zlo = -1, int zhi = -1) {
     Slab& s = h.slabs[slab_index];
-    const int nzl = s.zout_hi - s.zout_lo;
+    if (zlo < 0) {  // default: the slab's own output planes
+        zlo = s.zout_lo;
+        zhi = s.zout_hi;
+    }
+    const int nzl = zhi - zlo;
     const int max_grid = h.sm_count * occupancy_of(var);
     const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid);
     const int hx = tg.hx, OX = tg.ox;
@@ -886,8 +965,9 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.nzg = h.nz;
     p.tiles_x = tg.tiles_x;
     p.tiles_y = tg.tiles_y;
-    p.zout_lo = s.zout_lo;
-    p.zout_hi = s.zout_hi;
+    p.zout_lo = zlo;
+    p.zout_hi = zhi;
+    p.oz0 = s.zout_lo;  // the interior store map starts at the slab's first own plane
     p.nzc = tg.nzc;
     p.zc_len = tg.zc_len;
     p.units = tg.units;
@@ -1155,6 +1235,243 @@ void destroy(Handle* h) {
     delete h;
 }
 
+// ------------------------------------------------------------------------------------------
+// Streamed drop-in run (girih_gpu_run): the upload of the inputs, the fused passes and the
+// download of the results are pipelined along z.
+//
+// The whole run is cut into a skewed (z, t) task graph -- the wavefront idea of the reference
+// engine (engine.cpp:203-260) applied to the host link. Window c at pass p covers the interior
+// planes [z0(c) - off(p), z0(c+1) - off(p)), where off(p) is the sum of the fused depths H of
+// the earlier passes: each pass's window slides down by the distance its stencil cone reaches.
+// Task (c, p) then needs only (c, p-1) and (c-1, p-1) -- never the window above -- so the bottom
+// of the grid runs all its passes while the top is still crossing PCIe, and its results go back
+// while later inputs still come in. The levels rotate through three buffers of the source
+// parity, so a pass never overwrites planes an unfinished earlier pass still reads (WAR-free for
+// W >= 2H + 2; derivation in DESIGN.md). Only Jacobi kinds with TB = 2 passes (R = 1) qualify;
+// everything else runs the plain path (upload, girih_gpu_step, download).
+// ------------------------------------------------------------------------------------------
+bool stream_run_eligible(const Handle& h, long long steps) {
+    return h.slabs.size() == 1 && h.nranks == 1 && !h.emulated && h.kind != K_CONST25 &&
+           h.R == 1 && (h.cfg.tb == 0 || h.cfg.tb == 2) && steps >= 4 && h.nz >= 64 &&
+           !std::getenv("GIRIH_NO_STREAM_RUN");
+}
+
+void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu_report* rep) {
+    Slab& s = h.slabs[0];
+    GCHECK(cudaSetDevice(s.device));
+    const auto w0 = std::chrono::steady_clock::now();
+    const int b = parity_of(v.t_current);
+    const long long n2 = steps / 2;             // TB = 2 passes
+    const bool tail1 = (steps % 2) != 0;        // final single step
+    const int npass = int(n2) + (tail1 ? 1 : 0);
+    // window starts z0[c]: 64-plane windows (measured on var7pt 512^3, T = 100: 226 ms end to
+    // end vs 234-247 for 32 at the top, 281 for 32 everywhere, 236-270 for 80-128)
+    int WB = 64, WT = 64, TOPZ = 128;
+    if (const char* e = std::getenv("GIRIH_STREAM_W")) WB = WT = std::max(8, std::atoi(e));
+    const int W = 32;                           // upload chunk (allocated planes)
+    std::vector<int> off(npass + 1, 0), hp(npass, 2);
+    if (tail1) hp[npass - 1] = 1;
+    for (int q = 0; q < npass; ++q) off[q + 1] = off[q] + hp[q];
+    std::vector<int> z0{0};
+    while (z0.back() < h.nz + off[npass - 1])
+        z0.push_back(z0.back() + (z0.back() + WB <= h.nz - TOPZ ? WB : WT));
+    const int nwin = int(z0.size()) - 1;
+    const int plane_x = h.X, rows = h.Y;
+    const size_t hplane = size_t(plane_x) * rows;  // host doubles per allocated plane
+    const long long pe = h.plane_elems();
+
+    // buffers: three rotating buffers of parity b (the field of parity b + two scratch), the
+    // other field receives the odd-parity final level (penult or last single step)
+    std::unique_ptr<DevBuf> extra;
+    alloc_buf(s.buf[2 + b], s.device, h.slab_elems(s), s.stream);
+    alloc_buf(extra, s.device, h.slab_elems(s), s.stream);
+    double* rot[3] = {s.buf[b]->p, s.buf[2 + b]->p, extra->p};
+    double* other = s.buf[1 - b]->p;
+    std::unique_ptr<DevBuf> counters;
+    alloc_buf(counters, s.device, size_t(nwin) * npass + 1, s.stream);  // zeroed work counters
+    GCHECK(cudaStreamSynchronize(s.stream));
+    std::memcpy(h.cc, v.cc, sizeof h.cc);
+
+    // streams and events
+    cudaStream_t up = nullptr, down = nullptr;
+    std::vector<cudaStream_t> ws(nwin);
+    GCHECK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    GCHECK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    for (auto& x : ws) GCHECK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    const int nchunk = (h.Z + W - 1) / W;  // upload chunks of W allocated planes
+    std::vector<cudaEvent_t> ev_data(nchunk), ev_task(size_t(nwin) * npass);
+    for (auto& e : ev_data) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev_task) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t t_up0, t_up1, t_dn1;
+    GCHECK(cudaEventCreate(&t_up0));
+    GCHECK(cudaEventCreate(&t_up1));
+    GCHECK(cudaEventCreate(&t_dn1));
+    struct Cleanup {
+        cudaStream_t a, b;
+        std::vector<cudaStream_t>* ws;
+        std::vector<cudaEvent_t>* e1;
+        std::vector<cudaEvent_t>* e2;
+        cudaEvent_t x, y, z;
+        ~Cleanup() {
+            cudaStreamSynchronize(a);
+            cudaStreamSynchronize(b);
+            for (auto q : *ws) cudaStreamSynchronize(q), cudaStreamDestroy(q);
+            cudaStreamDestroy(a);
+            cudaStreamDestroy(b);
+            for (auto e : *e1) cudaEventDestroy(e);
+            for (auto e : *e2) cudaEventDestroy(e);
+            cudaEventDestroy(x);
+            cudaEventDestroy(y);
+            cudaEventDestroy(z);
+        }
+    } cleanup{up, down, &ws, &ev_data, &ev_task, t_up0, t_up1, t_dn1};
+
+    // ---- uploads, chunk by chunk in z: flat H2D into one of two staging blocks (stream `up`,
+    //      the PCIe copy engine) and the on-device 2-D scatter into the pitched layout on a
+    //      second stream, so the next H2D never waits for a scatter. The chunk of the parity-b
+    //      field is also copied into the two other rotating buffers (their ghost cells must
+    //      hold that parity's ghosts). ----
+    cudaStream_t scat = nullptr;
+    GCHECK(cudaStreamCreateWithFlags(&scat, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t st;
+        ~StreamGuard() {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    } scat_guard{scat};
+    std::unique_ptr<DevBuf> stage[2];
+    cudaEvent_t ev_h2d[2], ev_free[2];
+    for (int i = 0; i < 2; ++i) {
+        stage[i] = std::make_unique<DevBuf>();
+        stage[i]->alloc(s.device, size_t(W) * hplane * sizeof(double));
+        GCHECK(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming));
+        GCHECK(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
+    struct EventGuard {
+        cudaEvent_t* a;
+        cudaEvent_t* b;
+        ~EventGuard() {
+            for (int i = 0; i < 2; ++i) cudaEventDestroy(a[i]), cudaEventDestroy(b[i]);
+        }
+    } ev_guard{ev_h2d, ev_free};
+    GCHECK(cudaEventRecord(t_up0, up));
+    int nup = 0;
+    auto upload_chunk = [&](double* dev, const double* host, int k0, int nk) {
+        const int i = nup++ & 1;
+        if (nup > 2) GCHECK(cudaStreamWaitEvent(up, ev_free[i], 0));  // staging block reusable
+        GCHECK(cudaMemcpyAsync(stage[i]->p, host + size_t(k0) * hplane, size_t(nk) * hplane * 8,
+                               cudaMemcpyHostToDevice, up));
+        GCHECK(cudaEventRecord(ev_h2d[i], up));
+        GCHECK(cudaStreamWaitEvent(scat, ev_h2d[i], 0));
+        GCHECK(cudaMemcpy2DAsync(dev + (size_t)k0 * pe + h.off, size_t(h.pitch) * 8, stage[i]->p,
+                                 size_t(plane_x) * 8, size_t(plane_x) * 8, size_t(nk) * rows,
+                                 cudaMemcpyDeviceToDevice, scat));
+        GCHECK(cudaEventRecord(ev_free[i], scat));
+    };
+    for (int d = 0; d < nchunk; ++d) {
+        const int k0 = d * W, nk = std::min(W, h.Z - k0);
+        for (int c = 0; c < h.nc; ++c) upload_chunk(s.coeff(c, h.slab_elems(s)), v.coeffs[c], k0, nk);
+        upload_chunk(s.buf[b]->p, b == 0 ? v.u : v.v, k0, nk);
+        upload_chunk(other, b == 0 ? v.v : v.u, k0, nk);
+        for (int r = 1; r < 3; ++r)
+            GCHECK(cudaMemcpyAsync(rot[r] + (size_t)k0 * pe, rot[0] + (size_t)k0 * pe,
+                                   size_t(nk) * pe * 8, cudaMemcpyDeviceToDevice, scat));
+        GCHECK(cudaEventRecord(ev_data[d], scat));
+    }
+    GCHECK(cudaEventRecord(t_up1, scat));
+
+    // ---- compute tasks, issued window by window (the order the inputs arrive in: a task that
+    //      waits for late data never sits in a hardware queue ahead of a runnable one), each
+    //      window's results downloaded right after its last pass; every awaited event is
+    //      recorded before it is waited on ----
+    const Variant* var2 = select_variant(h.kind, 2, h.cfg.tb == 2 ? h.cfg.variant : -1);
+    const Variant* var1 = select_variant(h.kind, 1, -1);
+    long long computed = 0;
+    int launches = 0;
+    double* fin_b = tail1 ? rot[(npass - 1) % 3] : rot[npass % 3];  // final level of parity b
+    double* host_b = b == 0 ? v.u : v.v;
+    double* host_o = b == 0 ? v.v : v.u;
+    for (int c = 0; c < nwin; ++c) {
+      for (int q = 0; q < npass; ++q) {
+        const bool last = q == npass - 1;
+        const int tb = hp[q];
+        const Variant* var = tb == 2 ? var2 : var1;
+        Pass ps{tb, 0, -1, 0, -1};
+        double* src = rot[q % 3];
+        double* dst = (tail1 && last) ? other : rot[(q + 1) % 3];
+        double* pen = (!tail1 && last) ? other : nullptr;
+        const CUtensorMap& vmap = tensor_map(h, 0, src, 1, var->lx, var->ly);
+        const CUtensorMap& cmap =
+            h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.nc, var->aux_x, var->aux_y) : vmap;
+        {
+            const int lo = std::max(0, z0[c] - off[q]), hi = std::min(h.nz, z0[c + 1] - off[q]);
+            cudaEvent_t& mine = ev_task[size_t(c) * npass + q];
+            cudaStream_t st = ws[c];
+            if (q == 0) {  // inputs: planes up to the window top + H (+R allocated offset)
+                const int need = std::min(nchunk - 1, (z0[c + 1] + 2 + h.R) / W);
+                GCHECK(cudaStreamWaitEvent(st, ev_data[need], 0));
+            } else if (c > 0) {
+                GCHECK(cudaStreamWaitEvent(st, ev_task[size_t(c - 1) * npass + (q - 1)], 0));
+            }
+            if (hi > lo) {
+                LaunchInfo li;
+                PassParams p = build_params(h, ps, var, 0, v.t_current + 2LL * q, &li, h.R + lo,
+                                            h.R + hi);
+                p.src_prev = nullptr;
+                p.dst_final = dst;
+                p.dst_penult = pen;
+                p.work = reinterpret_cast<int*>(counters->p) + size_t(c) * npass + q;
+                p.work_base = 0;
+                const CUtensorMap& omap = tensor_map(h, 0, dst, 1, p.ox, var->ly - 2 * tb * h.R, 1);
+                GCHECK(var->launch(vmap, cmap, vmap, omap, p, li.grid, st));
+                computed += li.computed_lups;
+                ++launches;
+            }
+            GCHECK(cudaEventRecord(mine, st));
+        }
+      }
+      // this window's final planes go back as soon as its last pass is done
+      const int lo = std::max(0, z0[c] - off[npass - 1]), hi = std::min(h.nz, z0[c + 1] - off[npass - 1]);
+      if (hi <= lo) continue;
+      GCHECK(cudaStreamWaitEvent(down, ev_task[size_t(c) * npass + npass - 1], 0));
+      const int k0 = h.R + lo, nk = hi - lo;
+      for (int f = 0; f < 2; ++f) {
+          const double* dsrc = (f == 0 ? fin_b : other) + (size_t)k0 * pe + h.off;
+          double* hdst = (f == 0 ? host_b : host_o) + size_t(k0) * hplane;
+          GCHECK(cudaMemcpy2DAsync(hdst, size_t(plane_x) * 8, dsrc, size_t(h.pitch) * 8,
+                                   size_t(plane_x) * 8, size_t(nk) * rows,
+                                   cudaMemcpyDeviceToHost, down));
+      }
+    }
+    GCHECK(cudaEventRecord(t_dn1, down));
+    GCHECK(cudaEventSynchronize(t_dn1));
+    for (auto q : ws) GCHECK(cudaStreamSynchronize(q));
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    h.t_current = v.t_current + steps;
+    if (rep) {
+        std::memset(rep, 0, sizeof *rep);
+        float up_ms = 0, all_ms = 0;
+        GCHECK(cudaEventElapsedTime(&up_ms, t_up0, t_up1));
+        GCHECK(cudaEventElapsedTime(&all_ms, t_up0, t_dn1));
+        const size_t cells = size_t(h.X) * h.Y * h.Z;
+        rep->wall_s = wall;
+        rep->kernel_s = all_ms * 1e-3;  // device span of the pipelined upload/compute/download
+        rep->h2d_s = up_ms * 1e-3;
+        rep->d2h_s = 0;  // overlapped with the uploads and the passes
+        rep->lups = (long long)h.nx * h.ny * h.nz * steps;
+        rep->mlups = wall > 0 ? rep->lups / wall / 1e6 : 0.0;
+        rep->tb_used = 2;
+        rep->model_bytes_per_lup = double(kKinds[h.kind].b1) / 2;
+        rep->n_launches = launches;
+        rep->computed_lups = computed;
+        rep->h2d_bytes = (long long)(cells * 8 * (2 + h.nc));
+        rep->d2h_bytes = (long long)(size_t(h.X) * h.Y * h.nz * 8 * 2);
+        rep->variant_used = global_index_of(var2);
+        rep->streamed = 1;
+    }
+}
+
 double step_timed(Handle& h, long long steps, girih_gpu_report* rep) {
     const auto w0 = std::chrono::steady_clock::now();
     // device-clock timing: events around all work, per slab; take the max over slabs
@@ -1382,9 +1699,8 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
             GCHECK(cudaSetDevice(s.device));
             const double* dev = field < 2 ? s.buf[field]->p : s.coeff(field - 2, h.slab_elems(s));
             DevBuf blk, ctr;
-            blk.device = ctr.device = s.device;
-            GCHECK(cudaMalloc(&blk.p, size_t(std::min(bk, k1 - k0)) * plane_host * 8));
-            GCHECK(cudaMalloc(&ctr.p, 16));
+            blk.alloc(s.device, size_t(std::min(bk, k1 - k0)) * plane_host * 8);
+            ctr.alloc(s.device, 16);
             auto* cnt = reinterpret_cast<unsigned long long*>(ctr.p);
             const unsigned long long init[2] = {0ull, ~0ull};
             GCHECK(cudaMemcpyAsync(cnt, init, 16, cudaMemcpyHostToDevice, s.stream));
@@ -1474,6 +1790,26 @@ int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_conf
         setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
         validate_config(h->cfg, h->kind);
         setup_slabs(*h);
+        if (stream_run_eligible(*h, steps)) {
+            if (!state->u || !state->v) throw_err(GIRIH_EINVAL, "state view lacks u/v");
+            if (state->n_coeffs != h->nc)
+                throw_err(GIRIH_EINVAL, "coefficient field count does not match kind");
+            for (int c = 0; c < h->nc; ++c)
+                if (!state->coeffs || !state->coeffs[c])
+                    throw_err(GIRIH_EINVAL, "missing coefficient field");
+            girih_gpu_report r{};
+            stream_run(*h, *state, steps, &r);
+            state->t_current = h->t_current;
+            if (report) {
+                *report = r;
+                report->wall_s =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+                report->mlups = report->lups / report->wall_s / 1e6;
+            }
+            destroy(h);
+            h = nullptr;
+            return;
+        }
         const auto a0 = std::chrono::steady_clock::now();
         upload_state(*h, *state);
         const auto a1 = std::chrono::steady_clock::now();
@@ -1683,6 +2019,10 @@ int girih_gpu_slab_layout(int kind, int nz, int nslabs, int g, int* z0, int* z1,
         if (z1) *z1 = b;
         if (hz) *hz = nslabs == 1 ? k.radius : k.radius * max_tb(kind);
     });
+}
+
+int girih_gpu_trim(void) {
+    return guarded([&] { mem_cache_flush(-1); });
 }
 
 int girih_gpu_host_alloc(size_t bytes, void** ptr) {

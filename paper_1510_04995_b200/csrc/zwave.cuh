@@ -67,6 +67,7 @@ struct PassParams {
     int nzc, zc_len;         // z chunks per tile column and output planes per chunk
     int zout_lo, zout_hi;    // local output planes [lo, hi)
     int work_base;           // value of *work when this pass started (cumulative per step)
+    int oz0;                 // local plane of the output store map's z = 0 (the slab's zout_lo)
     int units;               // tiles_x * tiles_y * nzc
     int* work;               // dynamic unit counter (zeroed before every launch)
     unsigned long long* trace;  // optional per-iteration phase clocks of CTA 0 (debug)
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(NT, MINB)
                     pend = true;
                     pend_x = ug.tx * p.ox;
                     pend_y = ug.ty * OY;
-                    pend_z = j - H - p.zout_lo;
+                    pend_z = j - H - p.oz0;
                     pend_b = int(g % 3);
                 }
             }

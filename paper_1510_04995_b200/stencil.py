@@ -132,13 +132,14 @@ class PerfReport:
     variant_used: int = -1
     zchunks_used: int = 0
     grid_ctas: int = 0
+    streamed: int = 0  # girih_gpu_run pipelined the copies with the passes along z
 
     @staticmethod
     def from_c(r: GirihGpuReport) -> "PerfReport":
         return PerfReport(r.wall_s, r.kernel_s, r.lups, r.mlups / 1e3, r.mlups, r.h2d_s, r.d2h_s,
                           r.model_bytes_per_lup, r.tb_used, r.n_launches, r.pass_s,
                           r.computed_lups, r.h2d_bytes, r.d2h_bytes, r.variant_used,
-                          r.zchunks_used, r.grid_ctas)
+                          r.zchunks_used, r.grid_ctas, r.streamed)
 
 
 def variants():
@@ -239,6 +240,11 @@ def model(kind: int, grid: "GridSpec", tb: int = 0, variant: int = -1, hbm_gbs: 
     check(load().girih_gpu_model(int(kind), grid.nx, grid.ny, grid.nz, int(tb), int(variant),
                                  float(hbm_gbs), float(fp64_ops), C.byref(out)))
     return {name: getattr(out, name) for name, _ in GirihGpuModel._fields_}
+
+
+def trim() -> None:
+    """Release device memory cached between handles (girih_gpu_trim)."""
+    check(load().girih_gpu_trim())
 
 
 def pinned_empty(shape, dtype=np.float64) -> np.ndarray:

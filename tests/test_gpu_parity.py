@@ -284,3 +284,36 @@ def test_multi_tile_odd_extents(girih, oracle, kind):
             st = to_problem(g, base)
             g.run(st, steps, g.GpuConfig(tb=tb, emulate_slabs=nslab))
             assert_state_equal(st, ref, f"tb={tb} slabs={nslab}")
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=KIND_IDS[:2])
+def test_streamed_run_matches_oracle(girih, oracle, kind):
+    # girih_gpu_run's pipelined mode (uploads, skewed z-window passes and downloads overlapped):
+    # bitwise equal to the oracle for even/odd start levels, odd step counts (final single
+    # step), padding and grids that span several windows
+    g = girih
+    base = oracle.init_state(kind, 37, 29, 70, 2, 13, remap=True)
+    for t0, steps in ((0, 4), (0, 7), (1, 6), (1, 9), (0, 40), (1, 41)):
+        start = base.copy()
+        if t0:
+            oracle.naive_sweep(start, t0)
+        ref = start.copy()
+        oracle.naive_sweep(ref, steps)
+        st = to_problem(g, start)
+        rep = g.run(st, steps)
+        assert rep.streamed == 1
+        assert_state_equal(st, ref, f"streamed t0={t0} T={steps}")
+    # too few steps / explicit TB = 1: the plain path
+    st = to_problem(g, base)
+    assert g.run(st, 3).streamed == 0
+    assert g.run(st, 8, g.GpuConfig(tb=1)).streamed == 0
+
+
+def test_streamed_run_large(girih, oracle):
+    g = girih
+    base = oracle.init_state(0, 96, 80, 150, 0, 3, remap=True)
+    ref = base.copy()
+    oracle.naive_sweep(ref, 12)
+    st = to_problem(g, base)
+    assert g.run(st, 12).streamed == 1
+    assert_state_equal(st, ref, "streamed 96x80x150")

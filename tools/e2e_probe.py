@@ -17,9 +17,10 @@ for rep in range(3):
     t0 = time.perf_counter()
     pr = g.run(host, T, g.GpuConfig())
     t1 = time.perf_counter()
-    print(f"rep {rep}: call {1e3*(t1-t0):.1f} ms, wall {1e3*pr.wall_seconds:.1f} ms, h2d {1e3*pr.h2d_seconds:.1f} ms "
-          f"({pr.h2d_bytes/pr.h2d_seconds/1e9:.1f} GB/s), kernel {1e3*pr.kernel_seconds:.1f} ms, d2h {1e3*pr.d2h_seconds:.1f} ms "
-          f"({pr.d2h_bytes/pr.d2h_seconds/1e9:.1f} GB/s)")
+    print(f"rep {rep}: call {1e3*(t1-t0):.1f} ms, wall {1e3*pr.wall_seconds:.1f} ms ({pr.mlups:.0f} MLUP/s, "
+          f"streamed={pr.streamed}), h2d {1e3*pr.h2d_seconds:.1f} ms "
+          f"({pr.h2d_bytes/max(pr.h2d_seconds, 1e-9)/1e9:.1f} GB/s), kernel {1e3*pr.kernel_seconds:.1f} ms, "
+          f"d2h {1e3*pr.d2h_seconds:.1f} ms")
 # raw pinned copy bandwidth for comparison
 a = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
 b = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
