@@ -1250,10 +1250,15 @@ void destroy(Handle* h) {
 // W >= 2H + 2; derivation in DESIGN.md). Only Jacobi kinds with TB = 2 passes (R = 1) qualify;
 // everything else runs the plain path (upload, girih_gpu_step, download).
 // ------------------------------------------------------------------------------------------
+// Two modes: TB = 2 passes (R = 1 kinds at TB 0/2) rotate the levels through three buffers of
+// the source parity; single-step passes (R = 4, or TB = 1 requested) ping-pong u/v directly.
+// With the windows sliding by exactly the stencil reach H per pass, pass q of window c writes
+// up to where pass q-1 of window c+1 starts reading, and windows <= c-2 end >= W - 2H below,
+// so no pass overwrites planes an unfinished earlier pass still reads (W >= 2H).
 bool stream_run_eligible(const Handle& h, long long steps) {
     return h.slabs.size() == 1 && h.nranks == 1 && !h.emulated && h.kind != K_CONST25 &&
-           h.R == 1 && (h.cfg.tb == 0 || h.cfg.tb == 2) && steps >= 4 && h.nz >= 64 &&
-           !std::getenv("GIRIH_NO_STREAM_RUN");
+           (h.cfg.tb == 0 || h.cfg.tb == 1 || (h.cfg.tb == 2 && h.R == 1)) && steps >= 4 &&
+           h.nz >= 64 && !std::getenv("GIRIH_NO_STREAM_RUN");
 }
 
 void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu_report* rep) {
@@ -1261,17 +1266,18 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     GCHECK(cudaSetDevice(s.device));
     const auto w0 = std::chrono::steady_clock::now();
     const int b = parity_of(v.t_current);
-    const long long n2 = steps / 2;             // TB = 2 passes
-    const bool tail1 = (steps % 2) != 0;        // final single step
-    const int npass = int(n2) + (tail1 ? 1 : 0);
+    const bool single = h.R != 1 || h.cfg.tb == 1;  // single-step passes, u/v ping-pong
+    const long long n2 = single ? 0 : steps / 2;    // TB = 2 passes
+    const bool tail1 = !single && (steps % 2) != 0; // final single step
+    const int npass = single ? int(steps) : int(n2) + (tail1 ? 1 : 0);
     // window starts z0[c]: 64-plane windows (measured on var7pt 512^3, T = 100: 226 ms end to
     // end vs 234-247 for 32 at the top, 281 for 32 everywhere, 236-270 for 80-128)
     int WB = 64, WT = 64, TOPZ = 128;
     if (const char* e = std::getenv("GIRIH_STREAM_W")) WB = WT = std::max(8, std::atoi(e));
     const int W = 32;                           // upload chunk (allocated planes)
-    std::vector<int> off(npass + 1, 0), hp(npass, 2);
+    std::vector<int> off(npass + 1, 0), hp(npass, single ? 1 : 2);  // fused depth per pass
     if (tail1) hp[npass - 1] = 1;
-    for (int q = 0; q < npass; ++q) off[q + 1] = off[q] + hp[q];
+    for (int q = 0; q < npass; ++q) off[q + 1] = off[q] + hp[q] * h.R;  // window slide
     std::vector<int> z0{0};
     while (z0.back() < h.nz + off[npass - 1])
         z0.push_back(z0.back() + (z0.back() + WB <= h.nz - TOPZ ? WB : WT));
@@ -1280,12 +1286,16 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     const size_t hplane = size_t(plane_x) * rows;  // host doubles per allocated plane
     const long long pe = h.plane_elems();
 
-    // buffers: three rotating buffers of parity b (the field of parity b + two scratch), the
-    // other field receives the odd-parity final level (penult or last single step)
+    // buffers: TB = 2 mode: three rotating buffers of parity b (the field of parity b + two
+    // scratch), the other field receives the final level of the other parity (penult or the
+    // last single step); single-step mode: the two fields
     std::unique_ptr<DevBuf> extra;
-    alloc_buf(s.buf[2 + b], s.device, h.slab_elems(s), s.stream);
-    alloc_buf(extra, s.device, h.slab_elems(s), s.stream);
-    double* rot[3] = {s.buf[b]->p, s.buf[2 + b]->p, extra->p};
+    if (!single) {
+        alloc_buf(s.buf[2 + b], s.device, h.slab_elems(s), s.stream);
+        alloc_buf(extra, s.device, h.slab_elems(s), s.stream);
+    }
+    double* rot[3] = {s.buf[b]->p, single ? nullptr : s.buf[2 + b]->p,
+                      single ? nullptr : extra->p};
     double* other = s.buf[1 - b]->p;
     std::unique_ptr<DevBuf> counters;
     alloc_buf(counters, s.device, size_t(nwin) * npass + 1, s.stream);  // zeroed work counters
@@ -1374,7 +1384,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         for (int c = 0; c < h.nc; ++c) upload_chunk(s.coeff(c, h.slab_elems(s)), v.coeffs[c], k0, nk);
         upload_chunk(s.buf[b]->p, b == 0 ? v.u : v.v, k0, nk);
         upload_chunk(other, b == 0 ? v.v : v.u, k0, nk);
-        for (int r = 1; r < 3; ++r)
+        for (int r = 1; r < 3 && !single; ++r)
             GCHECK(cudaMemcpyAsync(rot[r] + (size_t)k0 * pe, rot[0] + (size_t)k0 * pe,
                                    size_t(nk) * pe * 8, cudaMemcpyDeviceToDevice, scat));
         GCHECK(cudaEventRecord(ev_data[d], scat));
@@ -1385,11 +1395,13 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     //      waits for late data never sits in a hardware queue ahead of a runnable one), each
     //      window's results downloaded right after its last pass; every awaited event is
     //      recorded before it is waited on ----
-    const Variant* var2 = select_variant(h.kind, 2, h.cfg.tb == 2 ? h.cfg.variant : -1);
-    const Variant* var1 = select_variant(h.kind, 1, -1);
+    const Variant* var2 =
+        single ? nullptr : select_variant(h.kind, 2, h.cfg.tb == 2 ? h.cfg.variant : -1);
+    const Variant* var1 = select_variant(h.kind, 1, h.cfg.tb == 1 ? h.cfg.variant : -1);
     long long computed = 0;
     int launches = 0;
-    double* fin_b = tail1 ? rot[(npass - 1) % 3] : rot[npass % 3];  // final level of parity b
+    // final level of parity b (single-step mode: the parity-b field itself)
+    double* fin_b = single ? rot[0] : tail1 ? rot[(npass - 1) % 3] : rot[npass % 3];
     double* host_b = b == 0 ? v.u : v.v;
     double* host_o = b == 0 ? v.v : v.u;
     for (int c = 0; c < nwin; ++c) {
@@ -1398,9 +1410,10 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         const int tb = hp[q];
         const Variant* var = tb == 2 ? var2 : var1;
         Pass ps{tb, 0, -1, 0, -1};
-        double* src = rot[q % 3];
-        double* dst = (tail1 && last) ? other : rot[(q + 1) % 3];
-        double* pen = (!tail1 && last) ? other : nullptr;
+        double* src = single ? s.buf[parity_of(v.t_current + q)]->p : rot[q % 3];
+        double* dst = single ? s.buf[parity_of(v.t_current + q + 1)]->p
+                             : (tail1 && last) ? other : rot[(q + 1) % 3];
+        double* pen = (!single && !tail1 && last) ? other : nullptr;
         const CUtensorMap& vmap = tensor_map(h, 0, src, 1, var->lx, var->ly);
         const CUtensorMap& cmap =
             h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.nc, var->aux_x, var->aux_y) : vmap;
@@ -1409,15 +1422,15 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
             cudaEvent_t& mine = ev_task[size_t(c) * npass + q];
             cudaStream_t st = ws[c];
             if (q == 0) {  // inputs: planes up to the window top + H (+R allocated offset)
-                const int need = std::min(nchunk - 1, (z0[c + 1] + 2 + h.R) / W);
+                const int need = std::min(nchunk - 1, (z0[c + 1] + hp[0] * h.R + h.R) / W);
                 GCHECK(cudaStreamWaitEvent(st, ev_data[need], 0));
             } else if (c > 0) {
                 GCHECK(cudaStreamWaitEvent(st, ev_task[size_t(c - 1) * npass + (q - 1)], 0));
             }
             if (hi > lo) {
                 LaunchInfo li;
-                PassParams p = build_params(h, ps, var, 0, v.t_current + 2LL * q, &li, h.R + lo,
-                                            h.R + hi);
+                PassParams p = build_params(h, ps, var, 0, v.t_current + (single ? q : 2LL * q),
+                                            &li, h.R + lo, h.R + hi);
                 p.src_prev = nullptr;
                 p.dst_final = dst;
                 p.dst_penult = pen;
@@ -1461,13 +1474,13 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         rep->d2h_s = 0;  // overlapped with the uploads and the passes
         rep->lups = (long long)h.nx * h.ny * h.nz * steps;
         rep->mlups = wall > 0 ? rep->lups / wall / 1e6 : 0.0;
-        rep->tb_used = 2;
-        rep->model_bytes_per_lup = double(kKinds[h.kind].b1) / 2;
+        rep->tb_used = single ? 1 : 2;
+        rep->model_bytes_per_lup = double(kKinds[h.kind].b1) / rep->tb_used;
         rep->n_launches = launches;
         rep->computed_lups = computed;
         rep->h2d_bytes = (long long)(cells * 8 * (2 + h.nc));
         rep->d2h_bytes = (long long)(size_t(h.X) * h.Y * h.nz * 8 * 2);
-        rep->variant_used = global_index_of(var2);
+        rep->variant_used = global_index_of(single ? var1 : var2);
         rep->streamed = 1;
     }
 }

@@ -303,10 +303,27 @@ def test_streamed_run_matches_oracle(girih, oracle, kind):
         rep = g.run(st, steps)
         assert rep.streamed == 1
         assert_state_equal(st, ref, f"streamed t0={t0} T={steps}")
-    # too few steps / explicit TB = 1: the plain path
+    # too few steps: the plain path
     st = to_problem(g, base)
     assert g.run(st, 3).streamed == 0
-    assert g.run(st, 8, g.GpuConfig(tb=1)).streamed == 0
+
+
+@pytest.mark.parametrize("kind,tb", [(3, 0), (0, 1), (1, 1)], ids=["var25pt", "const7pt-tb1",
+                                                                 "var7pt-tb1"])
+def test_streamed_run_single_step_passes(girih, oracle, kind, tb):
+    # the single-step streamed mode (u/v ping-pong, windows sliding by R per pass)
+    g = girih
+    base = oracle.init_state(kind, 33, 27, 80, 1, 17, remap=True)
+    for t0, steps in ((0, 4), (1, 7), (0, 13)):
+        start = base.copy()
+        if t0:
+            oracle.naive_sweep(start, t0)
+        ref = start.copy()
+        oracle.naive_sweep(ref, steps)
+        st = to_problem(g, start)
+        rep = g.run(st, steps, g.GpuConfig(tb=tb))
+        assert rep.streamed == 1 and rep.tb_used == 1
+        assert_state_equal(st, ref, f"streamed single t0={t0} T={steps}")
 
 
 def test_streamed_run_large(girih, oracle):
