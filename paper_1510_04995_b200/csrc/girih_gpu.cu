@@ -1255,9 +1255,14 @@ void destroy(Handle* h) {
 // With the windows sliding by exactly the stencil reach H per pass, pass q of window c writes
 // up to where pass q-1 of window c+1 starts reading, and windows <= c-2 end >= W - 2H below,
 // so no pass overwrites planes an unfinished earlier pass still reads (W >= 2H).
+// const25pt (leapfrog, single-step in place: level q+1 overwrites level q-1 cell by cell, as
+// kernels.hpp:50-52 do) streams in the single-step mode with the same windows: pass q of
+// window c writes level q+1 exactly up to where pass q-1 of window c+1 starts reading level q-1.
 bool stream_run_eligible(const Handle& h, long long steps) {
-    return h.slabs.size() == 1 && h.nranks == 1 && !h.emulated && h.kind != K_CONST25 &&
-           (h.cfg.tb == 0 || h.cfg.tb == 1 || (h.cfg.tb == 2 && h.R == 1)) && steps >= 4 &&
+    const bool tb_ok = h.kind == K_CONST25 ? (h.cfg.tb == 0 || h.cfg.tb == 1)
+                                           : (h.cfg.tb == 0 || h.cfg.tb == 1 ||
+                                              (h.cfg.tb == 2 && h.R == 1));
+    return h.slabs.size() == 1 && h.nranks == 1 && !h.emulated && tb_ok && steps >= 4 &&
            h.nz >= 64 && !std::getenv("GIRIH_NO_STREAM_RUN");
 }
 
@@ -1267,6 +1272,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     const auto w0 = std::chrono::steady_clock::now();
     const int b = parity_of(v.t_current);
     const bool single = h.R != 1 || h.cfg.tb == 1;  // single-step passes, u/v ping-pong
+    const bool leap = h.kind == K_CONST25;
     const long long n2 = single ? 0 : steps / 2;    // TB = 2 passes
     const bool tail1 = !single && (steps % 2) != 0; // final single step
     const int npass = single ? int(steps) : int(n2) + (tail1 ? 1 : 0);
@@ -1416,7 +1422,10 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         double* pen = (!single && !tail1 && last) ? other : nullptr;
         const CUtensorMap& vmap = tensor_map(h, 0, src, 1, var->lx, var->ly);
         const CUtensorMap& cmap =
-            h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.nc, var->aux_x, var->aux_y) : vmap;
+            h.nc > 0 ? tensor_map(h, 0, s.cblock->p, leap ? 1 : h.nc, var->aux_x, var->aux_y)
+                     : vmap;
+        // const25pt: level q-1 (read at the centre) lives in the destination field
+        const CUtensorMap& umap = leap ? tensor_map(h, 0, dst, 1, var->aux_x, var->aux_y) : vmap;
         {
             const int lo = std::max(0, z0[c] - off[q]), hi = std::min(h.nz, z0[c + 1] - off[q]);
             cudaEvent_t& mine = ev_task[size_t(c) * npass + q];
@@ -1431,13 +1440,13 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                 LaunchInfo li;
                 PassParams p = build_params(h, ps, var, 0, v.t_current + (single ? q : 2LL * q),
                                             &li, h.R + lo, h.R + hi);
-                p.src_prev = nullptr;
+                p.src_prev = leap ? dst : nullptr;
                 p.dst_final = dst;
                 p.dst_penult = pen;
                 p.work = reinterpret_cast<int*>(counters->p) + size_t(c) * npass + q;
                 p.work_base = 0;
                 const CUtensorMap& omap = tensor_map(h, 0, dst, 1, p.ox, var->ly - 2 * tb * h.R, 1);
-                GCHECK(var->launch(vmap, cmap, vmap, omap, p, li.grid, st));
+                GCHECK(var->launch(vmap, cmap, umap, omap, p, li.grid, st));
                 computed += li.computed_lups;
                 ++launches;
             }

@@ -308,8 +308,8 @@ def test_streamed_run_matches_oracle(girih, oracle, kind):
     assert g.run(st, 3).streamed == 0
 
 
-@pytest.mark.parametrize("kind,tb", [(3, 0), (0, 1), (1, 1)], ids=["var25pt", "const7pt-tb1",
-                                                                 "var7pt-tb1"])
+@pytest.mark.parametrize("kind,tb", [(3, 0), (2, 0), (0, 1), (1, 1)],
+                         ids=["var25pt", "const25pt", "const7pt-tb1", "var7pt-tb1"])
 def test_streamed_run_single_step_passes(girih, oracle, kind, tb):
     # the single-step streamed mode (u/v ping-pong, windows sliding by R per pass)
     g = girih
