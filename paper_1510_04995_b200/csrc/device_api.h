@@ -16,6 +16,12 @@ cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, i
                                  unsigned long long* count, unsigned long long* first,
                                  int sm_count, cudaStream_t stream);
 
+// ghost shell (ghost planes, ghost rows, ghost/pad columns) of allocated planes [k0, k0+nk) from
+// a packed host-order block (see init_kernels.cu)
+cudaError_t launch_scatter_shell(double* dev, int pitch, int off, int X, int Y, int R, int nx,
+                                 int ny, int nzg, int k0, int nk, const double* packed,
+                                 cudaStream_t stream);
+
 // mode 0: separate DMUL+DADD chains (2 ops per step), mode 1: DFMA chains (2 flops per step)
 cudaError_t launch_fp64_probe(int mode, double* out, int blocks, int threads, int iters,
                               cudaStream_t stream);

@@ -419,6 +419,25 @@ void dev_free(int device, void* p, size_t bytes) {
     cudaFree(p);
 }
 
+// process-wide pinned host scratch (grow-only; host-side packing for the streamed run, whose
+// callers hold pinned_scratch_mutex() for as long as they use it)
+std::mutex& pinned_scratch_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+double* pinned_scratch(size_t bytes) {
+    static void* p = nullptr;
+    static size_t have = 0;
+    if (bytes > have) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        have = 0;
+        GCHECK(cudaMallocHost(&p, bytes));
+        have = bytes;
+    }
+    return static_cast<double*>(p);
+}
+
 struct DevBuf {
     double* p = nullptr;
     int device = 0;
@@ -1267,11 +1286,13 @@ bool stream_run_eligible(const Handle& h, long long steps) {
 }
 
 void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu_report* rep) {
+    std::lock_guard<std::mutex> scratch_lock(pinned_scratch_mutex());  // one streamed run at a time
     Slab& s = h.slabs[0];
     GCHECK(cudaSetDevice(s.device));
     const auto w0 = std::chrono::steady_clock::now();
     const int b = parity_of(v.t_current);
-    const bool single = h.R != 1 || h.cfg.tb == 1;  // single-step passes, u/v ping-pong
+    const int tb_eff = h.cfg.tb > 0 ? h.cfg.tb : kKinds[h.kind].default_tb;
+    const bool single = h.R != 1 || tb_eff == 1;  // single-step passes, u/v ping-pong
     const bool leap = h.kind == K_CONST25;
     const long long n2 = single ? 0 : steps / 2;    // TB = 2 passes
     const bool tail1 = !single && (steps % 2) != 0; // final single step
@@ -1385,11 +1406,60 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                                  cudaMemcpyDeviceToDevice, scat));
         GCHECK(cudaEventRecord(ev_free[i], scat));
     };
+    // Jacobi kinds: the other field holds level t0-1, which no step reads (it is overwritten
+    // first), so only its ghost shell goes up: packed on the host chunk by chunk (overlapping
+    // the earlier chunks' transfers) and scattered on the device. const25pt reads it (leapfrog).
+    const bool shell = !leap;
+    const long long S_int = 2LL * h.R * h.X + (long long)h.ny * (h.X - h.nx);
+    auto shell_off = [&](int k) {  // packed doubles of allocated planes [0, k)
+        const long long g = std::min(k, h.R) + std::max(0, k - (h.R + h.nz));
+        return g * (long long)hplane + (long long)(k - g) * S_int;
+    };
+    const double* host_other = b == 0 ? v.v : v.u;
+    std::unique_ptr<DevBuf> dshell;
+    double* hshell = nullptr;
+    if (shell) {
+        dshell = std::make_unique<DevBuf>();
+        dshell->alloc(s.device, size_t(shell_off(h.Z)) * 8);
+        hshell = pinned_scratch(size_t(shell_off(h.Z)) * 8);
+    }
+    auto upload_shell = [&](int k0, int nk) {
+        double* o = hshell + shell_off(k0);
+        for (int k = k0; k < k0 + nk; ++k) {
+            const double* pl = host_other + size_t(k) * hplane;
+            if (k < h.R || k >= h.R + h.nz) {
+                std::memcpy(o, pl, hplane * 8);
+                o += hplane;
+                continue;
+            }
+            std::memcpy(o, pl, size_t(h.R) * h.X * 8);  // ghost rows at y < R
+            o += size_t(h.R) * h.X;
+            for (int j = h.R; j < h.R + h.ny; ++j) {        // ghost cells left / right (+ pad)
+                const double* r = pl + size_t(j) * h.X;
+                for (int i = 0; i < h.R; ++i) *o++ = r[i];
+                for (int i = h.R + h.nx; i < h.X; ++i) *o++ = r[i];
+            }
+            std::memcpy(o, pl + size_t(h.R + h.ny) * h.X, size_t(h.Y - h.R - h.ny) * h.X * 8);
+            o += size_t(h.Y - h.R - h.ny) * h.X;
+        }
+        const long long a = shell_off(k0), e = shell_off(k0 + nk);
+        GCHECK(cudaMemcpyAsync(dshell->p + a, hshell + a, size_t(e - a) * 8,
+                               cudaMemcpyHostToDevice, up));
+        const int i = nup++ & 1;  // reuse the staging events for ordering only
+        GCHECK(cudaEventRecord(ev_h2d[i], up));
+        GCHECK(cudaStreamWaitEvent(scat, ev_h2d[i], 0));
+        GCHECK(launch_scatter_shell(other, h.pitch, h.off, h.X, h.Y, h.R, h.nx, h.ny, h.nz, k0,
+                                    nk, dshell->p, scat));
+        GCHECK(cudaEventRecord(ev_free[i], scat));
+    };
     for (int d = 0; d < nchunk; ++d) {
         const int k0 = d * W, nk = std::min(W, h.Z - k0);
         for (int c = 0; c < h.nc; ++c) upload_chunk(s.coeff(c, h.slab_elems(s)), v.coeffs[c], k0, nk);
         upload_chunk(s.buf[b]->p, b == 0 ? v.u : v.v, k0, nk);
-        upload_chunk(other, b == 0 ? v.v : v.u, k0, nk);
+        if (shell)
+            upload_shell(k0, nk);
+        else
+            upload_chunk(other, host_other, k0, nk);
         for (int r = 1; r < 3 && !single; ++r)
             GCHECK(cudaMemcpyAsync(rot[r] + (size_t)k0 * pe, rot[0] + (size_t)k0 * pe,
                                    size_t(nk) * pe * 8, cudaMemcpyDeviceToDevice, scat));
@@ -1487,7 +1557,8 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         rep->model_bytes_per_lup = double(kKinds[h.kind].b1) / rep->tb_used;
         rep->n_launches = launches;
         rep->computed_lups = computed;
-        rep->h2d_bytes = (long long)(cells * 8 * (2 + h.nc));
+        rep->h2d_bytes = (long long)(cells * 8 * (shell ? 1 + h.nc : 2 + h.nc)) +
+                         (shell ? shell_off(h.Z) * 8 : 0);
         rep->d2h_bytes = (long long)(size_t(h.X) * h.Y * h.nz * 8 * 2);
         rep->variant_used = global_index_of(single ? var1 : var2);
         rep->streamed = 1;

@@ -88,6 +88,45 @@ cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, i
     return cudaGetLastError();
 }
 
+// ---- ghost shell of a field: scatter a packed [plane][shell] block into the device layout ----
+// Allocated planes [k0, k0 + nk) of a field whose interior is not needed (the input level t0-1
+// of a Jacobi run: overwritten before any read): ghost planes in full, in the other planes the
+// R ghost rows at each y end in full and, in every interior row, the R ghost cells left of the
+// interior and the R ghost + pad cells right of it. One block per (plane, row).
+__global__ void scatter_shell_kernel(double* dev, int pitch, int off, int X, int Y, int R, int nx,
+                                     int ny, int nzg, int k0, const double* packed) {
+    const int j = blockIdx.x, kk = blockIdx.y, k = k0 + kk;
+    const long long S = 2LL * R * X + (long long)ny * (X - nx);  // interior-plane shell
+    // packed offset of plane k: ghost planes before it are full planes
+    const int gbefore = min(k0, R) + max(0, k0 - (R + nzg));       // ghost planes before k0
+    const int ibefore = k0 - gbefore;                              // interior planes before k0
+    long long base = 0;
+    // planes of this chunk before k
+    for (int q = k0; q < k; ++q) base += (q < R || q >= R + nzg) ? (long long)X * Y : S;
+    base += (long long)gbefore * X * Y + (long long)ibefore * S;
+    double* row = dev + ((long long)k * Y + j) * pitch + off;
+    const bool gplane = k < R || k >= R + nzg;
+    if (gplane || j < R || j >= R + ny) {
+        const long long o = gplane ? base + (long long)j * X
+                                   : base + (j < R ? (long long)j * X
+                                                   : (long long)R * X + (long long)ny * (X - nx) +
+                                                         (long long)(j - R - ny) * X);
+        for (int i = threadIdx.x; i < X; i += blockDim.x) row[i] = packed[o + i];
+    } else {
+        const long long o = base + (long long)R * X + (long long)(j - R) * (X - nx);
+        for (int i = threadIdx.x; i < X - nx; i += blockDim.x)
+            row[i < R ? i : i + nx] = packed[o + i];
+    }
+}
+
+cudaError_t launch_scatter_shell(double* dev, int pitch, int off, int X, int Y, int R, int nx,
+                                 int ny, int nzg, int k0, int nk, const double* packed,
+                                 cudaStream_t stream) {
+    scatter_shell_kernel<<<dim3(Y, nk), 64, 0, stream>>>(dev, pitch, off, X, Y, R, nx, ny, nzg, k0,
+                                                         packed);
+    return cudaGetLastError();
+}
+
 // ---- FP64 rate probe: independent chains of DADD/DMUL (bitwise mode) or DFMA ----
 template <int MODE>
 __global__ void fp64_probe_kernel(double* out, int iters, double a, double b) {
