@@ -1481,25 +1481,17 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     double* host_b = b == 0 ? v.u : v.v;
     double* host_o = b == 0 ? v.v : v.u;
     for (int c = 0; c < nwin; ++c) {
-      for (int q = 0; q < npass; ++q) {
-        const bool last = q == npass - 1;
-        const int tb = hp[q];
-        const Variant* var = tb == 2 ? var2 : var1;
-        Pass ps{tb, 0, -1, 0, -1};
-        double* src = single ? s.buf[parity_of(v.t_current + q)]->p : rot[q % 3];
-        double* dst = single ? s.buf[parity_of(v.t_current + q + 1)]->p
-                             : (tail1 && last) ? other : rot[(q + 1) % 3];
-        double* pen = (!single && !tail1 && last) ? other : nullptr;
-        const CUtensorMap& vmap = tensor_map(h, 0, src, 1, var->lx, var->ly);
-        const CUtensorMap& cmap =
-            h.nc > 0 ? tensor_map(h, 0, s.cblock->p, leap ? 1 : h.nc, var->aux_x, var->aux_y)
-                     : vmap;
-        // const25pt: level q-1 (read at the centre) lives in the destination field
-        const CUtensorMap& umap = leap ? tensor_map(h, 0, dst, 1, var->aux_x, var->aux_y) : vmap;
-        {
+        cudaStream_t st = ws[c];
+        for (int q = 0; q < npass; ++q) {
+            const bool last = q == npass - 1;
+            const int tb = hp[q];
+            const Variant* var = tb == 2 ? var2 : var1;
+            const Pass ps{tb, 0, -1, 0, -1};
+            double* src = single ? s.buf[parity_of(v.t_current + q)]->p : rot[q % 3];
+            double* dst = single ? s.buf[parity_of(v.t_current + q + 1)]->p
+                                 : (tail1 && last) ? other : rot[(q + 1) % 3];
+            double* pen = (!single && !tail1 && last) ? other : nullptr;
             const int lo = std::max(0, z0[c] - off[q]), hi = std::min(h.nz, z0[c + 1] - off[q]);
-            cudaEvent_t& mine = ev_task[size_t(c) * npass + q];
-            cudaStream_t st = ws[c];
             if (q == 0) {  // inputs: planes up to the window top + H (+R allocated offset)
                 const int need = std::min(nchunk - 1, (z0[c + 1] + hp[0] * h.R + h.R) / W);
                 GCHECK(cudaStreamWaitEvent(st, ev_data[need], 0));
@@ -1507,6 +1499,13 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                 GCHECK(cudaStreamWaitEvent(st, ev_task[size_t(c - 1) * npass + (q - 1)], 0));
             }
             if (hi > lo) {
+                const CUtensorMap& vmap = tensor_map(h, 0, src, 1, var->lx, var->ly);
+                const CUtensorMap& cmap =
+                    h.nc > 0 ? tensor_map(h, 0, s.cblock->p, leap ? 1 : h.nc, var->aux_x, var->aux_y)
+                             : vmap;
+                // const25pt: level q-1 (read at the centre) lives in the destination field
+                const CUtensorMap& umap =
+                    leap ? tensor_map(h, 0, dst, 1, var->aux_x, var->aux_y) : vmap;
                 LaunchInfo li;
                 PassParams p = build_params(h, ps, var, 0, v.t_current + (single ? q : 2LL * q),
                                             &li, h.R + lo, h.R + hi);
@@ -1520,21 +1519,21 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                 computed += li.computed_lups;
                 ++launches;
             }
-            GCHECK(cudaEventRecord(mine, st));
+            GCHECK(cudaEventRecord(ev_task[size_t(c) * npass + q], st));
         }
-      }
-      // this window's final planes go back as soon as its last pass is done
-      const int lo = std::max(0, z0[c] - off[npass - 1]), hi = std::min(h.nz, z0[c + 1] - off[npass - 1]);
-      if (hi <= lo) continue;
-      GCHECK(cudaStreamWaitEvent(down, ev_task[size_t(c) * npass + npass - 1], 0));
-      const int k0 = h.R + lo, nk = hi - lo;
-      for (int f = 0; f < 2; ++f) {
-          const double* dsrc = (f == 0 ? fin_b : other) + (size_t)k0 * pe + h.off;
-          double* hdst = (f == 0 ? host_b : host_o) + size_t(k0) * hplane;
-          GCHECK(cudaMemcpy2DAsync(hdst, size_t(plane_x) * 8, dsrc, size_t(h.pitch) * 8,
-                                   size_t(plane_x) * 8, size_t(nk) * rows,
-                                   cudaMemcpyDeviceToHost, down));
-      }
+        // this window's final planes go back as soon as its last pass is done
+        const int lo = std::max(0, z0[c] - off[npass - 1]);
+        const int hi = std::min(h.nz, z0[c + 1] - off[npass - 1]);
+        if (hi <= lo) continue;
+        GCHECK(cudaStreamWaitEvent(down, ev_task[size_t(c) * npass + npass - 1], 0));
+        const int k0 = h.R + lo, nk = hi - lo;
+        for (int f = 0; f < 2; ++f) {
+            const double* dsrc = (f == 0 ? fin_b : other) + (size_t)k0 * pe + h.off;
+            double* hdst = (f == 0 ? host_b : host_o) + size_t(k0) * hplane;
+            GCHECK(cudaMemcpy2DAsync(hdst, size_t(plane_x) * 8, dsrc, size_t(h.pitch) * 8,
+                                     size_t(plane_x) * 8, size_t(nk) * rows,
+                                     cudaMemcpyDeviceToHost, down));
+        }
     }
     GCHECK(cudaEventRecord(t_dn1, down));
     GCHECK(cudaEventSynchronize(t_dn1));
