@@ -368,7 +368,11 @@ __global__ void __launch_bounds__(NT, MINB)
         for (int e = 0; e < P; ++e) issue_v();
         for (int e = 0; e < PA; ++e) issue_a();
     }
-    // output store pending from the previous iteration (thread 0)
+    // output store pending from the previous iteration. In CTAs of 2-8 warps (latency-bound:
+    // const7pt +4%, const25pt +3%) the output stores and their bulk-group waits run on warp 1
+    // (bulk groups are per thread), off the load producer's (thread 0's) per-plane critical
+    // path; the 14-warp var7pt TB=2 CTA keeps them on thread 0 (-2% otherwise)
+    constexpr int STORE_TID = (NT >= 64 && NT <= 256) ? 32 : 0;
     bool pend = false, stored_now = false;
     int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0;
 
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #endif
             unsigned long long* trp = tr ? p.trace + ((g - G0) * 2 + (tid == 32)) * 4 : nullptr;
             if (tr) trp[0] = clock64();
-            if (tid == 0) {
+            if (tid == STORE_TID) {
                 stored_now = false;
                 if (pend) {  // output plane of the previous iteration (staging fenced by writers)
                     tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
@@ -466,6 +470,8 @@ __global__ void __launch_bounds__(NT, MINB)
                     pend = false;
                     stored_now = true;
                 }
+            }
+            if (tid == 0) {
                 issue_v();
                 issue_a();
             }
@@ -731,10 +737,11 @@ __global__ void __launch_bounds__(NT, MINB)
                 }
             }
             if (tr) trp[2] = clock64();
-            // hand the staged output plane to the async proxy; thread 0 stores it next iteration
+            // hand the staged output plane to the async proxy; the store thread issues it next
+            // iteration
             if (staged) {
                 fence_proxy_async_smem();
-                if (tid == 0) {
+                if (tid == STORE_TID) {
                     pend = true;
                     pend_x = ug.tx * p.ox;
                     pend_y = ug.ty * OY;
@@ -744,7 +751,7 @@ __global__ void __launch_bounds__(NT, MINB)
             }
             // three staging planes: the plane the next iteration writes was handed to the store
             // issued two iterations ago, so only that older store must have finished reading
-            if (tid == 0) {
+            if (tid == STORE_TID) {
                 if (stored_now)
                     bulk_wait_read_but1();  // the store issued this iteration may stay in flight
                 else
@@ -754,7 +761,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == STORE_TID) {
         if (pend) {
             tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
             bulk_commit();
