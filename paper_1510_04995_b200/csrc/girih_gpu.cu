@@ -484,6 +484,7 @@ struct Handle {
     double cc[5] = {0, 0, 0, 0, 0};
     girih_gpu_config cfg{};
     int hz = 0;  // halo planes per slab side
+    bool uploads_all = false;  // girih_gpu_run: u, v and coefficients are uploaded before use
     std::vector<Slab> slabs;
     bool emulated = false;  // several slabs on one device
     // multi-process mode: this process owns slab `rank` of `nranks`; halos move over NCCL
@@ -564,12 +565,15 @@ void DevBuf::alloc(int dev, size_t n) {
     bytes = n;
 }
 
-void alloc_buf(std::unique_ptr<DevBuf>& b, int device, size_t elems, cudaStream_t st) {
+// zero = false: the caller overwrites every cell the kernels read (uploads of whole fields);
+// cells it leaves (row padding) only ever feed cells no valid cell reads
+void alloc_buf(std::unique_ptr<DevBuf>& b, int device, size_t elems, cudaStream_t st,
+               bool zero = true) {
     if (b) return;
     b = std::make_unique<DevBuf>();
     b->alloc(device, elems * sizeof(double));
     GCHECK(cudaSetDevice(device));
-    GCHECK(cudaMemsetAsync(b->p, 0, elems * sizeof(double), st));
+    if (zero) GCHECK(cudaMemsetAsync(b->p, 0, elems * sizeof(double), st));
 }
 
 void setup_geometry(Handle& h, int kind, int nx, int ny, int nz, int pad_x) {
@@ -663,9 +667,9 @@ void setup_slabs(Handle& h) {
         }
         GCHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         const size_t n = h.slab_elems(s);
-        alloc_buf(s.buf[0], s.device, n, s.stream);
-        alloc_buf(s.buf[1], s.device, n, s.stream);
-        if (h.nc > 0) alloc_buf(s.cblock, s.device, n * h.nc, s.stream);
+        alloc_buf(s.buf[0], s.device, n, s.stream, !h.uploads_all);
+        alloc_buf(s.buf[1], s.device, n, s.stream, !h.uploads_all);
+        if (h.nc > 0) alloc_buf(s.cblock, s.device, n * h.nc, s.stream, !h.uploads_all);
         alloc_buf(s.work, s.device, 32, s.stream);
     }
     if (!h.emulated && nslab > 1) {
@@ -1301,6 +1305,8 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     // end vs 234-247 for 32 at the top, 281 for 32 everywhere, 236-270 for 80-128)
     int WB = 64, WT = 64, TOPZ = 128;
     if (const char* e = std::getenv("GIRIH_STREAM_W")) WB = WT = std::max(8, std::atoi(e));
+    if (const char* e = std::getenv("GIRIH_STREAM_WT")) WT = std::max(8, std::atoi(e));
+    if (const char* e = std::getenv("GIRIH_STREAM_TOPZ")) TOPZ = std::max(0, std::atoi(e));
     const int W = 32;                           // upload chunk (allocated planes)
     std::vector<int> off(npass + 1, 0), hp(npass, single ? 1 : 2);  // fused depth per pass
     if (tail1) hp[npass - 1] = 1;
@@ -1318,8 +1324,8 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     // last single step); single-step mode: the two fields
     std::unique_ptr<DevBuf> extra;
     if (!single) {
-        alloc_buf(s.buf[2 + b], s.device, h.slab_elems(s), s.stream);
-        alloc_buf(extra, s.device, h.slab_elems(s), s.stream);
+        alloc_buf(s.buf[2 + b], s.device, h.slab_elems(s), s.stream, false);  // chunk copies
+        alloc_buf(extra, s.device, h.slab_elems(s), s.stream, false);
     }
     double* rot[3] = {s.buf[b]->p, single ? nullptr : s.buf[2 + b]->p,
                       single ? nullptr : extra->p};
@@ -1337,8 +1343,9 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     for (auto& x : ws) GCHECK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     const int nchunk = (h.Z + W - 1) / W;  // upload chunks of W allocated planes
     std::vector<cudaEvent_t> ev_data(nchunk), ev_task(size_t(nwin) * npass);
-    for (auto& e : ev_data) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : ev_task) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const unsigned evf = std::getenv("GIRIH_STREAM_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+    for (auto& e : ev_data) GCHECK(cudaEventCreateWithFlags(&e, evf));
+    for (auto& e : ev_task) GCHECK(cudaEventCreateWithFlags(&e, evf));
     cudaEvent_t t_up0, t_up1, t_dn1;
     GCHECK(cudaEventCreate(&t_up0));
     GCHECK(cudaEventCreate(&t_up1));
@@ -1538,6 +1545,17 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     GCHECK(cudaEventRecord(t_dn1, down));
     GCHECK(cudaEventSynchronize(t_dn1));
     for (auto q : ws) GCHECK(cudaStreamSynchronize(q));
+    if (std::getenv("GIRIH_STREAM_TRACE")) {  // diagnostics: when each window's passes ran
+        for (int c = 0; c < nwin; ++c) {
+            float a = 0, e = 0, d = 0;
+            const int need = std::min(nchunk - 1, (z0[c + 1] + hp[0] * h.R + h.R) / W);
+            cudaEventElapsedTime(&d, t_up0, ev_data[need]);
+            cudaEventElapsedTime(&a, t_up0, ev_task[size_t(c) * npass]);
+            cudaEventElapsedTime(&e, t_up0, ev_task[size_t(c) * npass + npass - 1]);
+            std::fprintf(stderr, "window %d [%d,%d): data %.1f ms, pass 1 done %.1f ms, last pass done %.1f ms\n",
+                         c, z0[c], z0[c + 1], d, a, e);
+        }
+    }
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
     h.t_current = v.t_current + steps;
     if (rep) {
@@ -1878,6 +1896,7 @@ int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_conf
         }
         const auto w0 = std::chrono::steady_clock::now();
         h = new Handle();
+        h->uploads_all = true;  // no zero-fill: every field is uploaded before any pass reads it
         h->cfg = cfg ? *cfg : default_config();
         setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
         validate_config(h->cfg, h->kind);
