@@ -7,20 +7,27 @@
 // through shared memory:
 //
 //   * level 0 (the input time level) arrives plane by plane by TMA (cp.async.bulk.tensor,
-//     box LX x LY x 1) into a ring of NR0 = 2R+1+P planes completed on mbarriers, P planes
-//     ahead of use -- the z-wavefront;
+//     box LX x LY x 1) into a ring of NR0 = R+1+P planes completed on mbarriers, P planes
+//     ahead of use -- the z-wavefront; thread 0 issues the loads, warp 1 the output stores;
 //   * the time-invariant coefficient fields (one contiguous [c][k][j][i] block) arrive by ONE
 //     4-D TMA per plane (box AX x AY x 1 x NC, the level-1 area) into an aux ring deep enough
 //     that level s re-uses the plane level 1 fetched (s-1)*R iterations earlier -- each
-//     coefficient byte crosses HBM once per pass, not once per fused step; const25pt's
-//     level t0-1 field rides in the same aux ring;
-//   * level s (1..TB) of plane k_s = j - s*R is computed at global iteration j from level
-//     s-1 planes k_s-R .. k_s+R: x/y/z neighbours come from the level-(s-1) smem ring, the
-//     newest plane (k_s+R) from the register the same thread produced one level earlier;
-//   * levels 1..TB-1 are kept in per-level rings of 2R+1 planes; level TB is stored to HBM;
+//     coefficient byte crosses HBM once per pass, not once per fused step (var7pt TB=2 carries
+//     level 1's coefficients to level 2 in registers instead); const25pt's level t0-1 field
+//     rides in the same aux ring;
+//   * a thread owns the same x-pairs of cells at every level (the rows [R, LY-R) of the tile);
+//     level s (1..TB) of plane k_s = j - s*R is computed at global iteration j from level
+//     s-1: x/y neighbours from the level-(s-1) centre plane in smem, z neighbours k_s-R ..
+//     k_s+R-1 from the thread's own register queue, k_s+R from the value it produced one
+//     level earlier in the same iteration;
+//   * levels 1..TB-1 keep rings of R+1 centre planes; level TB goes to a staging plane and
+//     out by a TMA store clipped to the interior (an odd nx's last column is stored directly);
 //   * the tile shrinks by R per side per level (overlapped / trapezoid tiling in x and y,
 //     and in z at z-chunk boundaries), so no inter-CTA synchronisation exists inside a pass;
-//     the x halo is H or H+1 so that every TMA box starts on a 16-byte boundary.
+//     the x halo is H or H+1 so that every TMA box starts on a 16-byte boundary;
+//   * work units (tile, z-chunk) are drawn dynamically in z-chunk-major order, which keeps
+//     neighbouring tiles within about a chunk of each other in z so shared halo rows are
+//     still in L2.
 //
 // One __syncthreads per z-plane orders every cross-thread smem dependency: all values a
 // level reads from smem were produced at least one iteration earlier.
