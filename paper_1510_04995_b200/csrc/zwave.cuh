@@ -253,10 +253,10 @@ struct ZwaveConfig {
     // loaded box are neighbours, never computed (for TB = 1 that is exactly the output rows)
     static constexpr int CR = LY - 2 * R;
     static constexpr int PPT = CR * LX / (2 * NT);  // x-pairs of cells per thread
-    // STACK (64-wide single-step tiles): a warp owns whole rows and a thread the same pair
-    // column in PPT consecutive rows, so the y neighbours of its pairs are one column window
-    // of PPT+2R pair loads instead of 2R loads per pair (radius 4: 46% fewer LDS.128)
-    static constexpr bool STACK = LX == 64 && TB == 1 && STACK_OK<KIND>::value;
+    // STACK (64-wide tiles, >= 2 pairs per thread): a warp owns whole rows and a thread the
+    // same pair column in PPT consecutive rows, so the y neighbours of its pairs are one column
+    // window of PPT+2R pair loads instead of 2R loads per pair (radius 4: 46% fewer LDS.128)
+    static constexpr bool STACK = LX == 64 && PPT >= 2 && STACK_OK<KIND>::value;
     static constexpr int XA = 2 * ((R + 1) / 2);  // pair-aligned x reach (R=1: 2, R=4: 4)
     static constexpr int NRING = NR0 + (TB - 1) * QL;
     // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
