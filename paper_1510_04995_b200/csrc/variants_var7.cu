@@ -11,8 +11,6 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT(K_VAR7, 1, 64, 16, 224, 4, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 2, 2, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 3, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 20, 576, 2, 1, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 20, 288, 2, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 18, 512, 2, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 18, 512, 3, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 224, 2, 2, 1),
