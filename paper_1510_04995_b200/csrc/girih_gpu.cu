@@ -425,14 +425,18 @@ std::mutex& pinned_scratch_mutex() {
     static std::mutex mu;
     return mu;
 }
-double* pinned_scratch(size_t bytes) {
+double* pinned_scratch(size_t bytes) {  // nullptr when no pinned memory can be had
     static void* p = nullptr;
     static size_t have = 0;
     if (bytes > have) {
         if (p) cudaFreeHost(p);
         p = nullptr;
         have = 0;
-        GCHECK(cudaMallocHost(&p, bytes));
+        if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return nullptr;
+        }
         have = bytes;
     }
     return static_cast<double*>(p);
@@ -1416,7 +1420,13 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     // Jacobi kinds: the other field holds level t0-1, which no step reads (it is overwritten
     // first), so only its ghost shell goes up: packed on the host chunk by chunk (overlapping
     // the earlier chunks' transfers) and scattered on the device. const25pt reads it (leapfrog).
-    const bool shell = !leap;
+    const size_t shell_bytes = [&] {
+        const long long g = 2LL * h.R;
+        return size_t(g * (long long)hplane +
+                      (long long)h.nz * (2LL * h.R * h.X + (long long)h.ny * (h.X - h.nx))) * 8;
+    }();
+    // without pinned scratch for the packed shell, upload the whole field instead
+    const bool shell = !leap && pinned_scratch(shell_bytes) != nullptr;
     const long long S_int = 2LL * h.R * h.X + (long long)h.ny * (h.X - h.nx);
     auto shell_off = [&](int k) {  // packed doubles of allocated planes [0, k)
         const long long g = std::min(k, h.R) + std::max(0, k - (h.R + h.nz));
