@@ -149,3 +149,17 @@ def test_model_matches_roofline_algebra(girih):
         girih.model(0, grid, 99)
     with pytest.raises(ValueError):
         girih.model(0, girih.GridSpec(2, 2, 2, 0), 1)
+
+
+def test_smoke_cases_use_compiled_depths(girih):
+    # __graft_entry__.smoke() must only request fused depths the library has kernels for
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("graft_entry", os.path.join(ROOT, "__graft_entry__.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    tbs = {(v["kind"], v["tb"]) for v in girih.variants()}
+    assert {k for k, _, _ in mod.SMOKE_CASES} == {0, 1, 2, 3}
+    for kind, tb, steps in mod.SMOKE_CASES:
+        assert (kind, tb) in tbs, (kind, tb)
+        assert steps % tb != 0 or steps // tb > 1
