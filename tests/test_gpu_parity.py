@@ -334,3 +334,45 @@ def test_streamed_run_large(girih, oracle):
     st = to_problem(g, base)
     assert g.run(st, 12).streamed == 1
     assert_state_equal(st, ref, "streamed 96x80x150")
+
+
+def test_randomised_configurations(girih, oracle):
+    # seeded fuzz over the configuration space the fixed cases do not enumerate: extents, pad,
+    # start level, step count, fused depth, variant, z chunks, emulated slabs, drop-in vs
+    # device-resident handle -- every result bitwise equal to the oracle, ghosts and pad included
+    g = girih
+    rng = np.random.default_rng(20261020)
+    by_kind = {}
+    for v in g.variants():
+        by_kind.setdefault(v["kind"], []).append(v)
+    for case in range(150):
+        kind = int(rng.integers(0, 4))
+        R = 1 if kind < 2 else 4
+        vs = by_kind[kind]
+        v = vs[int(rng.integers(0, len(vs)))]
+        tb = v["tb"]
+        lo = 2 * R + 1
+        nx, ny = (int(rng.integers(lo, lo + 45)) for _ in range(2))
+        nz = int(rng.integers(lo, lo + 40)) if rng.random() < 0.8 else int(rng.integers(64, 90))
+        pad = int(rng.integers(0, 4))
+        t0 = int(rng.integers(0, 3))
+        steps = int(rng.integers(0, 3 * tb + 4))
+        zc = int(rng.integers(0, 5))
+        slabs = int(rng.choice([0, 0, 0, 2, 3])) if nz >= 3 * (R * tb) + 3 else 0
+        base = oracle.init_state(kind, nx, ny, nz, pad, int(rng.integers(0, 1 << 30)),
+                                 remap=bool(rng.random() < 0.7))
+        if t0:
+            oracle.naive_sweep(base, t0)
+        ref = base.copy()
+        oracle.naive_sweep(ref, steps)
+        cfg = g.GpuConfig(tb=tb, variant=v["index"], zchunks=zc, emulate_slabs=slabs)
+        what = (f"case {case}: {KIND_IDS[kind]} {nx}x{ny}x{nz}+{pad} t0={t0} T={steps} tb={tb} "
+                f"variant={v['index']} zc={zc} slabs={slabs}")
+        if rng.random() < 0.5:
+            st = to_problem(g, base)
+            g.run(st, steps, cfg)
+        else:
+            with g.DeviceState.from_state(to_problem(g, base), cfg) as ds:
+                ds.step(steps)
+                st = ds.download()
+        assert_state_equal(st, ref, what)
