@@ -376,3 +376,23 @@ def test_randomised_configurations(girih, oracle):
                 ds.step(steps)
                 st = ds.download()
         assert_state_equal(st, ref, what)
+
+
+# interior checksums of the final level of BASELINE configs C2-C4 (512^3, T=100, seed 42, the
+# SURVEY 8(d) remap), probed with the reference engine itself
+REFERENCE_CONFIG_CHECKSUMS = [(1, 0xD2DF1C7A5D459BAC), (2, 0x7014FA6942240967),
+                              (3, 0x96F046612E0776C1)]
+
+
+@pytest.mark.parametrize("kind,want", REFERENCE_CONFIG_CHECKSUMS, ids=["C2", "C3", "C4"])
+def test_baseline_configs_match_reference_checksums(girih, kind, want):
+    # full-size parity where the CPU oracle would take minutes: the device-resident handle and
+    # the drop-in call (streamed) both reproduce the reference engine's checksum bit for bit
+    g = girih
+    with g.DeviceState.seeded(kind, g.GridSpec(512, 512, 512, 0), 42, remap=True) as ds:
+        init = ds.download(pinned=True)
+        ds.step(100)
+        assert g.interior_checksum(ds.download()) == want
+    rep = g.run(init, 100)
+    assert rep.streamed == 1
+    assert g.interior_checksum(init) == want
