@@ -396,3 +396,29 @@ def test_baseline_configs_match_reference_checksums(girih, kind, want):
     rep = g.run(init, 100)
     assert rep.streamed == 1
     assert g.interior_checksum(init) == want
+
+
+def test_streamed_run_randomised(girih, oracle):
+    # seeded fuzz of the streamed drop-in mode (grids tall enough to stream): every kind, start
+    # level, odd and even step counts, both pass modes, padding, odd extents
+    g = girih
+    rng = np.random.default_rng(7)
+    for case in range(30):
+        kind = int(rng.integers(0, 4))
+        R = 1 if kind < 2 else 4
+        tb = int(rng.choice([0, 1, 2])) if R == 1 else int(rng.choice([0, 1]))
+        nx, ny = (int(rng.integers(2 * R + 1, 2 * R + 50)) for _ in range(2))
+        nz = int(rng.integers(64, 150))
+        pad = int(rng.integers(0, 4))
+        t0 = int(rng.integers(0, 3))
+        steps = int(rng.integers(4, 31))
+        base = oracle.init_state(kind, nx, ny, nz, pad, int(rng.integers(0, 1 << 30)), remap=True)
+        if t0:
+            oracle.naive_sweep(base, t0)
+        ref = base.copy()
+        oracle.naive_sweep(ref, steps)
+        st = to_problem(g, base)
+        rep = g.run(st, steps, g.GpuConfig(tb=tb))
+        what = f"case {case}: {KIND_IDS[kind]} {nx}x{ny}x{nz}+{pad} t0={t0} T={steps} tb={tb}"
+        assert rep.streamed == 1, what
+        assert_state_equal(st, ref, what)
