@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GIRIH_GPU_ABI_VERSION 1
+#define GIRIH_GPU_ABI_VERSION 2
 
 #define GIRIH_OK 0
 #define GIRIH_EINVAL (-1)
@@ -67,7 +67,11 @@ typedef struct {
     int device;    /* CUDA device ordinal of the (first) GPU */
     int graphs;    /* >= 0: replay each step's pass sequence as a cached CUDA graph (single-
                       stream handles); -1 = launch passes individually */
-    int reserved;
+    int reserved;  /* >1: emulate that many z-slabs on one device (decomposition tests) */
+    int chain;     /* 1 = chain consecutive same-depth passes into one persistent launch whose
+                      work units start as soon as their neighbourhood finished the previous pass
+                      (single-slab handles); -1 = one launch per pass; 0 = auto (chained for
+                      grids of at most 2^22 cells, where the per-pass ramp-up and tail matter) */
 } girih_gpu_config;
 
 typedef struct {
@@ -87,6 +91,7 @@ typedef struct {
     int grid_ctas;
     int streamed;           /* girih_gpu_run: 1 = uploads, passes and downloads pipelined along z
                                (skewed task graph; kernel_s is then the whole device span) */
+    int n_passes;           /* stencil passes (a chained launch runs several) */
 } girih_gpu_report;
 
 /* kernel variant description (compiled tile shapes) */

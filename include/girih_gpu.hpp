@@ -31,6 +31,8 @@ struct GpuConfig {
     int ngpus = 1;     // z-slab decomposition across devices [device, device + ngpus)
     int device = 0;
     int graphs = 0;
+    int chain = 0;     // 1 = chain same-depth passes into one dependency-driven launch; -1 = off;
+                       // 0 = auto (small grids)
 };
 
 // PerfReport (engine.hpp:93-98) plus the GPU-side timings.
@@ -57,6 +59,7 @@ inline girih_gpu_config to_c(const GpuConfig& c) {
     o.exact = 1;
     o.device = c.device;
     o.graphs = c.graphs;
+    o.chain = c.chain;
     return o;
 }
 

@@ -37,6 +37,7 @@ class GirihGpuConfig(C.Structure):
     _fields_ = [
         ("tb", C.c_int), ("variant", C.c_int), ("zchunks", C.c_int), ("ngpus", C.c_int),
         ("exact", C.c_int), ("device", C.c_int), ("graphs", C.c_int), ("reserved", C.c_int),
+        ("chain", C.c_int),
     ]
 
 
@@ -49,7 +50,7 @@ class GirihGpuReport(C.Structure):
         ("pass_s", C.c_double), ("computed_lups", C.c_longlong),
         ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong),
         ("variant_used", C.c_int), ("zchunks_used", C.c_int), ("grid_ctas", C.c_int),
-        ("streamed", C.c_int),
+        ("streamed", C.c_int), ("n_passes", C.c_int),
     ]
 
 

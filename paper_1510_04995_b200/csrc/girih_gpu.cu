@@ -455,7 +455,7 @@ struct DevBuf {
 };
 
 struct StepStats {
-    int n_launches = 0;
+    int n_launches = 0, n_passes = 0;
     double pass_s = 0;
     long long computed = 0;
     int grid = 0, zchunks = 0, variant = -1, tb_used = 0;
@@ -472,6 +472,8 @@ struct Slab {
     std::unique_ptr<DevBuf> buf[4];     // u, v, scratch even, scratch odd
     std::unique_ptr<DevBuf> cblock;     // coefficient fields, contiguous [c][k][j][i]
     std::unique_ptr<DevBuf> work;       // dynamic work counters of the zwave launches
+    std::unique_ptr<DevBuf> chain_done; // chained launches: finished tiles per (pass, z chunk)
+    size_t chain_done_ints = 0;
     std::unique_ptr<DevBuf> trace;      // GIRIH_TRACE: per-iteration phase clocks (debug)
     std::unique_ptr<DevBuf> hstage;     // flat staging for host copies (one field, X-pitched)
     bool hstage_failed = false;         // no memory for it: copy 2-D straight from the host
@@ -506,7 +508,7 @@ struct Handle {
     std::vector<std::unique_ptr<MapEntry>> maps;
     struct GraphEntry {
         long long parity = 0, steps = 0;
-        int tb = 0, variant = 0, zchunks = 0;
+        int tb = 0, variant = 0, zchunks = 0, chain = 0;
         bool timed = false;
         cudaGraphExec_t exec = nullptr;
         StepStats st;
@@ -1073,6 +1075,25 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
             if (b >= 2) ensure_scratch(h, b & 1);
     }
+    // pass chaining (single-slab handles): per-(pass, z chunk) tile counters, allocated
+    // before any graph capture
+    // auto (chain = 0): small grids only. A chained launch removes the per-pass ramp-up and
+    // tail (~20 us per pass; +24..48% at 64^3-128^3), but its kernel carries the dependency and
+    // publication state and runs 10-30% slower per unit, which loses from 256^3 on (measured,
+    // DESIGN.md section 4b)
+    const long long cells = (long long)h.nx * h.ny * h.nz;
+    const bool want_chain = h.cfg.chain > 0 || (h.cfg.chain == 0 && cells <= (1ll << 22));
+    const bool can_chain = want_chain && h.slabs.size() == 1 && h.nranks == 1 &&
+                           !std::getenv("GIRIH_TRACE") && !std::getenv("GIRIH_NO_CHAIN");
+    if (can_chain) {
+        Slab& s = h.slabs[0];
+        const size_t need = size_t(CHAIN_MAX) * size_t(std::max(1, s.zout_hi - s.zout_lo));
+        if (s.chain_done_ints < need) {
+            s.chain_done.reset();
+            alloc_buf(s.chain_done, s.device, (need + 1) / 2, s.stream);
+            s.chain_done_ints = need;
+        }
+    }
     if (time_passes) {
         const size_t need = 2 * plan.size();
         GCHECK(cudaSetDevice(h.slabs[0].device));
@@ -1090,7 +1111,8 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     if (use_graph) {
         for (auto& e : h.graphs)
             if (e.parity == parity_of(h.t_current) && e.steps == steps && e.tb == tb &&
-                e.variant == h.cfg.variant && e.zchunks == h.cfg.zchunks && e.timed == time_passes)
+                e.variant == h.cfg.variant && e.zchunks == h.cfg.zchunks &&
+                e.chain == h.cfg.chain && e.timed == time_passes)
                 ge = &e;
         if (ge) {
             GCHECK(cudaSetDevice(h.slabs[0].device));
@@ -1134,12 +1156,84 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         GCHECK(cudaSetDevice(s.device));
         GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
     }
-    for (const Pass& ps : plan) {
+    for (size_t pidx = 0; pidx < plan.size(); ++pidx) {
+        const Pass& ps = plan[pidx];
         const Variant* var =
             select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
         if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
         st.variant = global_index_of(var);
         st.tb_used = std::max(st.tb_used, ps.tb);
+        if (can_chain) {
+            // the longest run of passes with this depth (same variant and tile grid) that fits
+            // one launch: <= CHAIN_MAX passes, <= CHAIN_DESC distinct buffer sets
+            std::vector<std::array<int, 5>> keys;
+            std::vector<int> idx;
+            long long tq = t;
+            size_t e = pidx;
+            for (; e < plan.size() && plan[e].tb == ps.tb && e - pidx < size_t(CHAIN_MAX); ++e) {
+                const Pass& pe = plan[e];
+                const std::array<int, 5> key{pe.src, pe.src_prev, pe.dst, pe.dst_penult,
+                                             parity_of(tq)};
+                size_t k = 0;
+                while (k < keys.size() && keys[k] != key) ++k;
+                if (k == keys.size()) {
+                    if (keys.size() == size_t(CHAIN_DESC)) break;
+                    keys.push_back(key);
+                }
+                idx.push_back(int(k));
+                tq += pe.tb;
+            }
+            Slab& s = h.slabs[0];
+            LaunchInfo li;
+            PassParams p = build_params(h, ps, var, 0, t, &li);
+            // a unit reads z chunks +-1 of the previous pass only if its halo fits in a chunk
+            if (e - pidx >= 2 && ps.tb * h.R <= p.zc_len) {
+                const int npass = int(e - pidx);
+                GCHECK(cudaSetDevice(s.device));
+                ChainDescs cd{};
+                long long tk = t;
+                for (size_t k = 0; k < keys.size(); ++k) {
+                    // the first pass using buffer set k (its parity is part of the key)
+                    size_t f = pidx;
+                    tk = t;
+                    while (idx[f - pidx] != int(k)) tk += plan[f++].tb;
+                    const Pass& pf = plan[f];
+                    PassDesc& d = cd.d[k];
+                    d.vmap = tensor_map(h, 0, s.buf[pf.src]->p, 1, var->lx, var->ly);
+                    d.umap = pf.src_prev >= 0 ? tensor_map(h, 0, s.buf[pf.src_prev]->p, 1,
+                                                           var->aux_x, var->aux_y)
+                                              : d.vmap;
+                    d.omap = tensor_map(h, 0, s.buf[pf.dst]->p, 1, p.ox, var->ly - 2 * pf.tb * h.R, 1);
+                    d.dst_final = s.buf[pf.dst]->p;
+                    d.dst_penult = pf.dst_penult >= 0 ? s.buf[pf.dst_penult]->p : nullptr;
+                    d.parity0 = parity_of(tk);
+                }
+                for (int q = 0; q < npass; ++q) cd.pidx[q] = (unsigned char)idx[q];
+                cd.npass = npass;
+                cd.done = reinterpret_cast<int*>(s.chain_done->p);
+                GCHECK(cudaMemsetAsync(cd.done, 0, size_t(npass) * p.nzc * sizeof(int), s.stream));
+                p.work_base = int(work_base[0]);
+                work_base[0] += (long long)npass * p.units;
+                const CUtensorMap& cmap =
+                    h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc,
+                                          var->aux_x, var->aux_y)
+                             : cd.d[0].vmap;
+                const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+                if (time_passes) GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
+                GCHECK(var->launch_chain(cmap, cd, p, li.grid, s.stream));
+                if (time_passes) GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
+                st.computed += li.computed_lups * npass;
+                st.grid = li.grid;
+                st.zchunks = li.zchunks;
+                st.n_launches++;
+                st.n_passes += npass;
+                for (int q = 0; q < npass; ++q) t += plan[pidx + q].tb;
+                pidx += npass - 1;
+                ++pi;
+                continue;
+            }
+        }
+        st.n_passes++;
         for (size_t g = 0; g < h.slabs.size(); ++g) {
             Slab& s = h.slabs[g];
             GCHECK(cudaSetDevice(s.device));
@@ -1201,6 +1295,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         e.tb = tb;
         e.variant = h.cfg.variant;
         e.zchunks = h.cfg.zchunks;
+        e.chain = h.cfg.chain;
         e.timed = time_passes;
         e.st = st;
         const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
@@ -1583,6 +1678,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         rep->tb_used = single ? 1 : 2;
         rep->model_bytes_per_lup = double(kKinds[h.kind].b1) / rep->tb_used;
         rep->n_launches = launches;
+        rep->n_passes = launches;
         rep->computed_lups = computed;
         rep->h2d_bytes = (long long)(cells * 8 * (shell ? 1 + h.nc : 2 + h.nc)) +
                          (shell ? shell_off(h.Z) * 8 : 0);
@@ -1628,6 +1724,7 @@ double step_timed(Handle& h, long long steps, girih_gpu_report* rep) {
         rep->tb_used = st.tb_used;
         rep->model_bytes_per_lup = st.tb_used > 0 ? double(ki.b1) / st.tb_used : 0.0;
         rep->n_launches = st.n_launches;
+        rep->n_passes = st.n_passes;
         rep->pass_s = st.pass_s;
         rep->computed_lups = st.computed;
         rep->variant_used = st.variant;

@@ -82,6 +82,33 @@ struct PassParams {
                              // innermost box coordinate 16-byte aligned (even for fp64)
 };
 
+// Pass chaining. One launch may run a sequence of passes over the same tile grid. Units are
+// numbered pass-major (U = q * units + u) and drawn in that order; a unit of pass q > 0 starts
+// once every unit that wrote a plane it reads, or reads a plane it overwrites, has finished
+// pass q-1 (chain_deps_ready). This is the device counterpart of the reference's
+// dependency-counting TileScheduler (proj/src/scheduler.cpp:18-102): no grid-wide barrier and
+// no kernel boundary between passes, so no per-pass ramp-up and tail. Deadlock-free because
+// every dependency points at a unit drawn earlier and every drawn unit belongs to a resident
+// CTA (persistent grid of at most occupancy x SMs CTAs).
+constexpr int CHAIN_DESC = 6;   // distinct per-pass buffer sets in one launch
+constexpr int CHAIN_MAX = 128;  // passes in one launch
+
+struct PassDesc {               // what changes from pass to pass
+    CUtensorMap vmap;           // level-0 source buffer (3-D)
+    CUtensorMap umap;           // const25pt: level t0-1 (3-D)
+    CUtensorMap omap;           // output: interior of dst_final
+    double* dst_final;          // level t0+TB (odd-nx last column stored directly)
+    double* dst_penult;         // level t0+TB-1 or nullptr
+    int parity0;                // parity of t0
+};
+
+struct ChainDescs {
+    PassDesc d[CHAIN_DESC];         // single-pass launches use d[0] only
+    unsigned char pidx[CHAIN_MAX];  // pass q uses d[pidx[q]]
+    int npass;
+    int* done;                      // tiles finished per (pass, z chunk), zeroed per launch
+};
+
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -190,44 +217,88 @@ constexpr int UQ = 8;  // unit queue depth (the producer runs at most a few unit
 
 struct Cursor {
     int seq;   // this CTA's unit sequence number
-    int u;     // unit id (>= units: exhausted)
+    int u;     // unit id (>= total: exhausted); chained: q * units + ul
+    int q;     // pass of the unit within a chained launch (0 otherwise)
     int it, n_it;
     UnitGeom ug;
 };
 
-template <int H>
-__device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int seq, int u) {
+// u: chained unit id q * units + ul (total = npass * units; single-pass launches: q = 0)
+template <int H, bool CHAIN>
+__device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int total, int seq,
+                                           int u) {
     c.seq = seq;
     c.u = u;
     c.it = 0;
     c.n_it = 0;
-    if (u < p.units) {
-        c.ug = unit_geom(p, u);
+    c.q = 0;
+    if (u < total) {
+        if (CHAIN) c.q = u / p.units;
+        c.ug = unit_geom(p, u - c.q * p.units);
         c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
     }
 }
 
 // advance within / across units; the drawing cursor (V producer) fetches new unit ids
-template <int H, bool DRAW>
-__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, volatile int* uq,
-                                            int* drawn) {
+template <int H, bool CHAIN, bool DRAW>
+__device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, int total,
+                                            volatile int* uq, int* drawn) {
     if (++c.it >= c.n_it) {
         int next;
         if (DRAW) {
             // the id drawn at the start of this unit; draw the one after it now, so the atomic's
             // latency hides behind a whole unit instead of stalling the producer warp
             next = *drawn;
-            if (next < p.units) {
+            if (next < total) {
                 const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
-                *drawn = d < p.units ? d : p.units;
+                *drawn = d < total ? d : total;
             }
             uq[(c.seq + 1) % UQ] = next;
         } else {
             next = uq[(c.seq + 1) % UQ];
         }
-        cursor_set<H>(c, p, c.seq + 1, next);
+        cursor_set<H, CHAIN>(c, p, total, c.seq + 1, next);
     }
 }
+
+// Pass chaining: done[q * nzc + zc] counts the tiles that finished chunk zc of pass q. Unit
+// (tile, zc) of pass q may start once chunk rows zc-1 .. zc+1 of pass q-1 are complete: they
+// hold every unit that wrote a plane it reads or reads a plane it overwrites (the halo H is at
+// most one chunk). Whole rows rather than the 3 x 3 tile neighbourhood: 3 polls instead of
+// 27, and units are drawn z-chunk-major, so a row is long finished when the next pass
+// reaches it.
+__device__ __forceinline__ bool chain_deps_ready(const PassParams& p, const int* done, int q,
+                                                 int ul) {
+    const int txy = p.tiles_x * p.tiles_y;
+    const int zc = ul / txy;
+    const int* row = done + (q - 1) * p.nzc;
+    int a, b, c;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(a) : "l"(row + max(zc - 1, 0)));
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(b) : "l"(row + zc));
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(c) : "l"(row + min(zc + 1, p.nzc - 1)));
+#ifdef GIRIH_CHAIN_NODEPS
+    return true;  // timing experiment only: no ordering between passes (results are wrong)
+#endif
+    return min(a, min(b, c)) >= txy;
+}
+
+// makes a finished unit visible (TMA stores complete, direct stores ordered by the CTA
+// barrier) before its row count; the reader fences after observing the count
+__device__ __forceinline__ void chain_publish(const PassParams& p, int* done, int u) {
+    const int q = u / p.units, ul = u - q * p.units;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    // release: the CTA's earlier writes (ordered before this thread by the CTA barrier and,
+    // for the TMA stores, by the completed bulk groups and the proxy fence) happen-before it
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(
+                     done + q * p.nzc + ul / (p.tiles_x * p.tiles_y))
+                 : "memory");
+}
+__device__ __forceinline__ void chain_acquire() {
+    // pairs with the release above through the relaxed reads of the counters
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 
 template <int KIND> struct STACK_OK { static constexpr bool value = true; };
 
@@ -287,12 +358,13 @@ struct ZwaveConfig {
     static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
+// CHAIN = false: one pass (descriptors d[0]); true: cd.npass chained passes. The two are
+// separate instantiations so that single-pass launches carry none of the chaining state (the
+// 128-register var7pt CTA spills otherwise, and shared-memory producer state cost 30%).
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN>
 __global__ void __launch_bounds__(NT, MINB)
-    zwave_kernel(const __grid_constant__ CUtensorMap vmap,  // level-0 source buffer (3-D)
-                 const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
-                 const __grid_constant__ CUtensorMap umap,  // const25pt: level t0-1 (3-D)
-                 const __grid_constant__ CUtensorMap omap,  // output: interior of dst_final
+    zwave_kernel(const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
+                 const __grid_constant__ ChainDescs cd,     // per-pass buffers and maps
                  const __grid_constant__ PassParams p) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
@@ -326,23 +398,50 @@ __global__ void __launch_bounds__(NT, MINB)
 
     // ---- producers (thread 0): V runs P elements ahead, aux PA elements ahead ----
     __shared__ int uq[UQ];
+    const int total = CHAIN ? cd.npass * p.units : p.units;  // units of the launch
     Cursor vcur{}, acur{};
     uint32_t vnext = G0, anext = G0;
     int drawn = 0;  // producer: next unit id, drawn one unit ahead
-    auto issue_v = [&]() {
-        if (vcur.u >= p.units) return;
+    // chained launches: the V cursor's unit passed its dependency check; the store thread's
+    // finished unit whose last plane is the pending store
+    bool vready = false;
+    int pub_next = -1;
+    // returns false when a chained unit's dependencies are not met yet and `must` is false
+    auto issue_v = [&](bool must) -> bool {
+        if (vcur.u >= total) return false;
+        if constexpr (CHAIN) {
+            if (vcur.it == 0 && vcur.q > 0 && !vready) {
+                const int ul = vcur.u - vcur.q * p.units;
+                if (!chain_deps_ready(p, cd.done, vcur.q, ul)) {
+                    if (!must) return false;  // retry next iteration
+                    // the consumer needs this plane now. If this CTA's own last unit is a
+                    // dependency, the store thread publishes it at the top of this same
+                    // iteration (before the barrier this thread is held at), so the wait ends.
+                    long long spins = 0;
+                    while (!chain_deps_ready(p, cd.done, vcur.q, ul)) {
+                        __nanosleep(128);
+                        if (++spins > (1ll << 25)) __trap();  // never hang the GPU on a bug
+                    }
+                }
+                chain_acquire();
+                vready = true;
+            }
+        }
         const int j = vcur.ug.za - H + vcur.it;
         const int slot = int(vnext % NR0);
         const int xd = p.off + vcur.ug.tx * p.ox + R - p.hx;  // even by construction
         const int yd = vcur.ug.ty * OY + R - H;
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
-        tma_load_plane(ring0 + slot * CELLS, &vmap, xd, yd, j, &vbar[slot]);
+        tma_load_plane(ring0 + slot * CELLS, &cd.d[CHAIN ? cd.pidx[vcur.q] : 0].vmap, xd, yd, j,
+                       &vbar[slot]);
         ++vnext;
-        cursor_next<H, true>(vcur, p, uq, &drawn);
+        cursor_next<H, CHAIN, true>(vcur, p, total, uq, &drawn);
+        if (CHAIN && vcur.it == 0) vready = false;
+        return true;
     };
     auto issue_a = [&]() {
         if constexpr (NAUX > 0) {
-            if (acur.u >= p.units) return;
+            if (acur.u >= total) return;
             const int k1 = acur.ug.za - H + acur.it - R;  // level-1 plane of that iteration
             const int slot = int(anext % NAR);
             const int xd = p.off + acur.ug.tx * p.ox + R - p.hx + AXO;
@@ -352,43 +451,48 @@ __global__ void __launch_bounds__(NT, MINB)
                 // the phase without moving data
                 mbar_arrive(&abar[slot]);
                 ++anext;
-                cursor_next<H, false>(acur, p, uq, nullptr);
+                cursor_next<H, CHAIN, false>(acur, p, total, uq, nullptr);
                 return;
             }
             mbar_arrive_expect_tx(&abar[slot], AUX_BYTES);
             double* dst = auxr + slot * AUXPLANE;
             if constexpr (KIND == K_CONST25) {
                 tma_load_plane(dst, &cmap, xd, yd, k1, &abar[slot]);
-                tma_load_plane(dst + AYX, &umap, xd, yd, k1, &abar[slot]);
+                tma_load_plane(dst + AYX, &cd.d[CHAIN ? cd.pidx[acur.q] : 0].umap, xd, yd, k1,
+                               &abar[slot]);
             } else {
                 tma_load_4d(dst, &cmap, xd, yd, k1, 0, &abar[slot]);
             }
             ++anext;
-            cursor_next<H, false>(acur, p, uq, nullptr);
+            cursor_next<H, CHAIN, false>(acur, p, total, uq, nullptr);
         }
     };
     static_assert(P >= PA, "the V producer draws units and must lead the aux producer");
     if (tid == 0) {
-        const int u0 = blockIdx.x < p.units ? int(blockIdx.x) : p.units;
+        // the first unit is blockIdx.x: grid <= units, so in a chain it belongs to pass 0
+        const int u0 = blockIdx.x < total ? int(blockIdx.x) : total;
         uq[0] = u0;
-        if (u0 < p.units) {
+        if (u0 < total) {
             const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
-            drawn = d < p.units ? d : p.units;
+            drawn = d < total ? d : total;
         } else {
-            drawn = p.units;
+            drawn = total;
         }
-        cursor_set<H>(vcur, p, 0, u0);
-        cursor_set<H>(acur, p, 0, u0);
-        for (int e = 0; e < P; ++e) issue_v();
-        for (int e = 0; e < PA; ++e) issue_a();
+        cursor_set<H, CHAIN>(vcur, p, total, 0, u0);
+        cursor_set<H, CHAIN>(acur, p, total, 0, u0);
+        if constexpr (!CHAIN) {  // chained launches issue from the first iteration on
+            for (int e = 0; e < P; ++e) issue_v(true);
+            for (int e = 0; e < PA; ++e) issue_a();
+        }
     }
     // output store pending from the previous iteration. In CTAs of 2-8 warps (latency-bound:
     // const7pt +4%, const25pt +3%) the output stores and their bulk-group waits run on warp 1
     // (bulk groups are per thread), off the load producer's (thread 0's) per-plane critical
-    // path; the 14-warp var7pt TB=2 CTA keeps them on thread 0 (-2% otherwise)
+    // path; the 14-warp var7pt TB=2 CTA keeps them on thread 0 (-2% otherwise). In chained
+    // launches the store thread also publishes finished units (bulk groups are per thread).
     constexpr int STORE_TID = (NT >= 64 && NT <= 256) ? 32 : 0;
     bool pend = false, stored_now = false;
-    int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0;
+    int pend_x = 0, pend_y = 0, pend_z = 0, pend_b = 0, pend_q = 0;
 
     // ---- per-thread constants. A thread owns x-PAIRS of cells (2 consecutive x): every
     //      neighbour access is a 16-byte LDS.128 and the x neighbourhood of a pair comes from
@@ -422,7 +526,18 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
         for (int i = 0; i < PPT; ++i)
             if (__all_sync(0xffffffffu, dyv[i] < s * R)) wskip |= 1u << ((s - 1) * PPT + i);
-    const bool has_penult = p.dst_penult != nullptr;
+    // a chained unit's pass-dependent values, read where needed (rare paths) from shared
+    // memory instead of being held in registers by every thread
+    struct UnitState {
+        const double* ghost_s[TB + 1];  // parity-(t0+s) pristine field (ghost values of level s)
+        double* dst_final;
+        double* dst_penult;
+        int u, q;
+    };
+    // double-buffered by unit sequence: slower warps may still read the previous unit's copy
+    // in its last iteration while thread 0 fills the next one (no barrier in between)
+    __shared__ UnitState SU2[2];
+    const bool has_penult_1 = p.dst_penult != nullptr;  // single-pass launches
     // coefficient queue (CQ): cq[L][pair] = coefficients level 1 used L+1 iterations ago
     constexpr int CQD = CQ ? TB - 1 : 1, CQN = CQ ? 7 : 1;
     double2 cq[CQD][PPT][CQN], cnew[PPT][CQN];
@@ -439,8 +554,21 @@ __global__ void __launch_bounds__(NT, MINB)
     uint32_t g = G0;  // consumer's global element index
     for (int seq = 0;; ++seq) {
         const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
-        if (u >= p.units) break;
-        const UnitGeom ug = unit_geom(p, u);
+        if (u >= total) break;
+        const UnitGeom ug = unit_geom(p, CHAIN ? u % p.units : u);
+        UnitState& SU = SU2[seq & 1];
+        if constexpr (CHAIN) {
+            if (tid == 0) {  // published by the __syncthreads_or below
+                const int q = u / p.units;
+                const PassDesc& pd = cd.d[cd.pidx[q]];
+#pragma unroll
+                for (int s2 = 0; s2 <= TB; ++s2) SU.ghost_s[s2] = p.ghost[(pd.parity0 + s2) & 1];
+                SU.dst_final = pd.dst_final;
+                SU.dst_penult = pd.dst_penult;
+                SU.u = u;
+                SU.q = q;
+            }
+        }
         const int n_it = (ug.zb - ug.za) + 2 * H;
         const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
         const int ya0 = ug.ty * OY + R - H;
@@ -481,15 +609,35 @@ __global__ void __launch_bounds__(NT, MINB)
             if (tid == STORE_TID) {
                 stored_now = false;
                 if (pend) {  // output plane of the previous iteration (staging fenced by writers)
-                    tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
+                    tma_store_plane(&cd.d[CHAIN ? cd.pidx[pend_q] : 0].omap, stage + pend_b * STAGE,
+                                    pend_x, pend_y, pend_z);
                     bulk_commit();
                     pend = false;
                     stored_now = true;
                 }
+                if constexpr (CHAIN) {
+                    // a finished unit (its last plane was just stored) is published as soon as
+                    // its stores have completed: the producer may be waiting for it right now
+                    if (pub_next >= 0) {
+                        bulk_wait_all();
+                        chain_publish(p, cd.done, pub_next);
+                        pub_next = -1;
+                    }
+                }
             }
             if (tid == 0) {
-                issue_v();
-                issue_a();
+                if constexpr (CHAIN) {
+                    // V planes up to g + P (at least plane g, which the consumer waits for
+                    // next), aux planes up to g + PA but never past V, which checks a unit's
+                    // dependencies before its first plane
+                    while (vnext <= g + P)
+                        if (!issue_v(vnext <= g)) break;
+                    if constexpr (NAUX > 0)
+                        while (anext <= g + PA && anext < vnext) issue_a();
+                } else {
+                    issue_v(true);
+                    issue_a();
+                }
             }
             // ghost values of the intermediate levels this iteration (boundary tiles and ghost
             // planes only), loaded before the TMA waits so their latency overlaps them. Level TB
@@ -502,7 +650,8 @@ __global__ void __launch_bounds__(NT, MINB)
                 const int kg = k + p.zoff;
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
                 if (!(plane_ghost || any_ghost_col)) continue;
-                const double* ghost = p.ghost[(p.parity0 + s) & 1] + (long long)k * p.plane;
+                const double* ghost =
+                    (CHAIN ? SU.ghost_s[s] : p.ghost[(p.parity0 + s) & 1]) + (long long)k * p.plane;
                 const uint32_t fix = plane_ghost ? ok_mask : col_fix;
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
@@ -712,15 +861,16 @@ __global__ void __launch_bounds__(NT, MINB)
                         if ((out_mask >> (2 * i + 1)) & 1) stg[sidx[i] + 1] = val[i].y;
                     }
                     if (any_odd_col && k >= p.zout_lo && k < p.zout_hi) {
-                        double* dst = p.dst_final + (long long)k * p.plane;
+                        double* dst = (CHAIN ? SU.dst_final : p.dst_final) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
                             if ((odd_mask >> (2 * i)) & 1) dst[colidx[2 * i]] = val[i].x;
                             if ((odd_mask >> (2 * i + 1)) & 1) dst[colidx[2 * i + 1]] = val[i].y;
                         }
                     }
-                    if (has_penult) {  // final pass only: level TB-1 of the same cells
-                        double* pen = p.dst_penult + (long long)k * p.plane;
+                    if (CHAIN ? SU.dst_penult != nullptr : has_penult_1) {  // final pass only:
+                        // level TB-1 of the same cells
+                        double* pen = (CHAIN ? SU.dst_penult : p.dst_penult) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
                             const double2 c2 = zq[TB - 1][i][R];  // level TB-1 at plane k
@@ -775,8 +925,11 @@ __global__ void __launch_bounds__(NT, MINB)
                     pend_y = ug.ty * OY;
                     pend_z = j - H - p.oz0;
                     pend_b = int(g % 3);
+                    if constexpr (CHAIN) pend_q = SU.q;
                 }
             }
+            if constexpr (CHAIN)
+                if (tid == STORE_TID && it == n_it - 1) pub_next = SU.u;  // unit finished
             // three staging planes: the plane the next iteration writes was handed to the store
             // issued two iterations ago, so only that older store must have finished reading
             if (tid == STORE_TID) {
@@ -791,10 +944,13 @@ __global__ void __launch_bounds__(NT, MINB)
     __syncthreads();
     if (tid == STORE_TID) {
         if (pend) {
-            tma_store_plane(&omap, stage + pend_b * STAGE, pend_x, pend_y, pend_z);
+            tma_store_plane(&cd.d[CHAIN ? cd.pidx[pend_q] : 0].omap, stage + pend_b * STAGE, pend_x,
+                            pend_y, pend_z);
             bulk_commit();
         }
         bulk_wait_all();
+        if constexpr (CHAIN)  // other CTAs may be waiting for this CTA's last unit
+            if (pub_next >= 0) chain_publish(p, cd.done, pub_next);
     }
 }
 

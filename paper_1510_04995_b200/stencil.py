@@ -107,10 +107,12 @@ class GpuConfig:
     device: int = 0
     graphs: int = 0
     emulate_slabs: int = 0  # >1: that many z-slabs on ONE device (decomposition tests)
+    chain: int = 0       # 1: chain same-depth passes into one dependency-driven launch; -1: off;
+                         # 0: auto (grids of at most 2^22 cells)
 
     def to_c(self) -> GirihGpuConfig:
         return GirihGpuConfig(self.tb, self.variant, self.zchunks, self.ngpus, 1, self.device,
-                              self.graphs, self.emulate_slabs)
+                              self.graphs, self.emulate_slabs, self.chain)
 
 
 @dataclass
@@ -133,13 +135,14 @@ class PerfReport:
     zchunks_used: int = 0
     grid_ctas: int = 0
     streamed: int = 0  # girih_gpu_run pipelined the copies with the passes along z
+    n_passes: int = 0  # stencil passes (a chained launch runs several)
 
     @staticmethod
     def from_c(r: GirihGpuReport) -> "PerfReport":
         return PerfReport(r.wall_s, r.kernel_s, r.lups, r.mlups / 1e3, r.mlups, r.h2d_s, r.d2h_s,
                           r.model_bytes_per_lup, r.tb_used, r.n_launches, r.pass_s,
                           r.computed_lups, r.h2d_bytes, r.d2h_bytes, r.variant_used,
-                          r.zchunks_used, r.grid_ctas, r.streamed)
+                          r.zchunks_used, r.grid_ctas, r.streamed, r.n_passes)
 
 
 def variants():
@@ -370,7 +373,7 @@ class DeviceState:
         check(load().girih_gpu_tune(self._handle(), int(max_tb), C.byref(best), C.byref(mlups),
                                     C.byref(n)))
         cfg = GpuConfig(best.tb, best.variant, best.zchunks, best.ngpus, best.device, best.graphs,
-                        best.reserved)
+                        best.reserved, best.chain)
         return cfg, mlups.value, n.value
 
     def close(self) -> None:

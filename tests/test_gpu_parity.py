@@ -422,3 +422,64 @@ def test_streamed_run_randomised(girih, oracle):
         what = f"case {case}: {KIND_IDS[kind]} {nx}x{ny}x{nz}+{pad} t0={t0} T={steps} tb={tb}"
         assert rep.streamed == 1, what
         assert_state_equal(st, ref, what)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_chained_passes_match_oracle(girih, oracle, kind):
+    # pass chaining (one persistent launch per run of same-depth passes, units gated by the
+    # per-(pass, z chunk) completion counters) against the oracle and against one launch per
+    # pass: every compiled depth, several z-chunkings (incl. the fewest chunks a halo allows),
+    # start parities and step counts that mix depths in one plan
+    g = girih
+    dims = (45, 38, 52, 1) if kind < 2 else (41, 35, 47, 0)
+    base = oracle.init_state(kind, *dims, 23, remap=True)
+    r = TRAITS[kind][0]
+    for tb in tbs_for(g, kind):
+        for zc in (0, 1, 3, max(1, dims[2] // (tb * r)), dims[2]):  # last: halo > chunk
+            for t0_steps, steps in ((0, 4 * tb + 1), (1, 3 * tb)):
+                ref = base.copy()
+                oracle.naive_sweep(ref, t0_steps + steps)
+                st = to_problem(g, base)
+                if t0_steps:
+                    g.run(st, t0_steps, g.GpuConfig(chain=-1))
+                rep = g.run(st, steps, g.GpuConfig(tb=tb, zchunks=zc, chain=1))
+                what = f"{KIND_IDS[kind]} tb={tb} zc={zc} t0={t0_steps} T={steps}"
+                assert_state_equal(st, ref, what)
+                assert rep.n_passes >= rep.n_launches, what
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_chained_tiny_grids_self_dependencies(girih, oracle, kind):
+    # fewer units per pass than resident CTAs: a CTA's next unit often depends on the unit it
+    # is finishing (its own publication must come first), and whole passes overlap
+    g = girih
+    r = TRAITS[kind][0]
+    for n in (2 * r + 1, 2 * r + 4, 16):
+        base = oracle.init_state(kind, n, n + 1, n + 2, 0, 3, remap=True)
+        for tb in tbs_for(g, kind):
+            steps = 6 * tb + 1
+            ref = base.copy()
+            oracle.naive_sweep(ref, steps)
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb, chain=1))
+            assert_state_equal(st, ref, f"{KIND_IDS[kind]} n={n} tb={tb}")
+
+
+def test_chained_device_state_long_runs(girih, oracle):
+    # a long chain (more passes than one launch holds: CHAIN_MAX = 128) on a device handle,
+    # bitwise equal to one launch per pass; the report counts passes and launches
+    g = girih
+    for kind in (0, 3):
+        grid = g.GridSpec(24, 20, 28, 0)
+        outs = {}
+        for chain in (1, -1):
+            with g.DeviceState.seeded(kind, grid, 7, remap=True,
+                                      config=g.GpuConfig(tb=1, chain=chain)) as ds:
+                rep = ds.step(300)
+                st = ds.download(coeffs=False)
+                outs[chain] = (st.u.copy(), st.v.copy(), rep)
+        assert np.array_equal(outs[1][0].view(np.uint64), outs[-1][0].view(np.uint64))
+        assert np.array_equal(outs[1][1].view(np.uint64), outs[-1][1].view(np.uint64))
+        rc, rp = outs[1][2], outs[-1][2]
+        assert rc.n_passes == rp.n_passes == 300
+        assert rp.n_launches == 300 and rc.n_launches == 3  # 128 + 128 + 44
