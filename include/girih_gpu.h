@@ -71,7 +71,7 @@ typedef struct {
     int chain;     /* 1 = chain consecutive same-depth passes into one persistent launch whose
                       work units start as soon as their neighbourhood finished the previous pass
                       (single-slab handles); -1 = one launch per pass; 0 = auto (chained for
-                      grids of at most 2^22 cells, where the per-pass ramp-up and tail matter) */
+                      grids of at most 256^3 cells, except var7pt) */
 } girih_gpu_config;
 
 typedef struct {

@@ -932,7 +932,16 @@ struct TileGeom {
     long long computed_lups;
 };
 
-TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max_grid) {
+// Chained launches balance load across the whole pass sequence, not per pass, so their z
+// chunks need not be short: 8 chunks per column (>= 8 planes and >= the halo), measured best on
+// 128^3-256^3 (const7pt 256^3: 282 K MLUP/s at 8 chunks, 254 K at 16, 230 K at 4).
+int choose_zchunks_chained(int nzl, int H) {
+    const int len = std::max({8, H, (nzl + 7) / 8});
+    return std::max(1, (nzl + len - 1) / len);
+}
+
+TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max_grid,
+                   bool chained = false) {
     TileGeom t{};
     const int R = h.R, H = tb * R;
     // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
@@ -943,6 +952,7 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
     t.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
+            : chained         ? choose_zchunks_chained(nzl, H)
                               : choose_zchunks(nzl, H, h.nc, txy, max_grid);
     t.zc_len = (nzl + t.nzc - 1) / t.nzc;
     t.nzc = (nzl + t.zc_len - 1) / t.zc_len;
@@ -961,7 +971,8 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
 
 // Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
 PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_index,
-                        long long t0, LaunchInfo* li, int zlo = -1, int zhi = -1) {
+                        long long t0, LaunchInfo* li, int zlo = -1, int zhi = -1,
+                        bool chained = false) {
     Slab& s = h.slabs[slab_index];
     if (zlo < 0) {  // default: the slab's own output planes
         zlo = s.zout_lo;
@@ -969,7 +980,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     }
     const int nzl = zhi - zlo;
     const int max_grid = h.sm_count * occupancy_of(var);
-    const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid);
+    const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid, chained);
     const int hx = tg.hx, OX = tg.ox;
     PassParams p{};
     p.hx = hx;
@@ -1077,12 +1088,15 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     }
     // pass chaining (single-slab handles): per-(pass, z chunk) tile counters, allocated
     // before any graph capture
-    // auto (chain = 0): small grids only. A chained launch removes the per-pass ramp-up and
-    // tail (~20 us per pass; +24..48% at 64^3-128^3), but its kernel carries the dependency and
-    // publication state and runs 10-30% slower per unit, which loses from 256^3 on (measured,
-    // DESIGN.md section 4b)
+    // auto (chain = 0): grids of at most 256^3 cells, except var7pt. A chained launch removes
+    // the per-pass ramp-up and tail (~20 us per pass) and allows long z chunks (fewer re-read
+    // halo planes), but its kernel carries the dependency and publication state: it wins up
+    // to 256^3 (const7pt +13%, var25pt 128^3 +38%) and loses at 512^3 (-3..-9%). The chained
+    // var7pt kernel spills at the 448-thread CTA's 128-register cap and always loses (DESIGN.md
+    // section 4b).
     const long long cells = (long long)h.nx * h.ny * h.nz;
-    const bool want_chain = h.cfg.chain > 0 || (h.cfg.chain == 0 && cells <= (1ll << 22));
+    const bool want_chain =
+        h.cfg.chain > 0 || (h.cfg.chain == 0 && cells <= (1ll << 24) && h.kind != K_VAR7);
     const bool can_chain = want_chain && h.slabs.size() == 1 && h.nranks == 1 &&
                            !std::getenv("GIRIH_TRACE") && !std::getenv("GIRIH_NO_CHAIN");
     if (can_chain) {
@@ -1185,7 +1199,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             }
             Slab& s = h.slabs[0];
             LaunchInfo li;
-            PassParams p = build_params(h, ps, var, 0, t, &li);
+            PassParams p = build_params(h, ps, var, 0, t, &li, -1, -1, true);
             // a unit reads z chunks +-1 of the previous pass only if its halo fits in a chunk
             if (e - pidx >= 2 && ps.tb * h.R <= p.zc_len) {
                 const int npass = int(e - pidx);

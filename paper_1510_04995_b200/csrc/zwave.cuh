@@ -532,7 +532,6 @@ __global__ void __launch_bounds__(NT, MINB)
         const double* ghost_s[TB + 1];  // parity-(t0+s) pristine field (ghost values of level s)
         double* dst_final;
         double* dst_penult;
-        int u, q;
     };
     // double-buffered by unit sequence: slower warps may still read the previous unit's copy
     // in its last iteration while thread 0 fills the next one (no barrier in between)
@@ -556,17 +555,18 @@ __global__ void __launch_bounds__(NT, MINB)
         const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
         if (u >= total) break;
         const UnitGeom ug = unit_geom(p, CHAIN ? u % p.units : u);
-        UnitState& SU = SU2[seq & 1];
+        // chained: bit 0 = the unit's pass writes the penult level, bits 1.. = that pass
+        int uflags = 0;
         if constexpr (CHAIN) {
+            const int q = u / p.units;
+            const PassDesc& pd = cd.d[cd.pidx[q]];
+            uflags = (q << 1) | (pd.dst_penult != nullptr ? 1 : 0);
             if (tid == 0) {  // published by the __syncthreads_or below
-                const int q = u / p.units;
-                const PassDesc& pd = cd.d[cd.pidx[q]];
+                UnitState& SU = SU2[seq & 1];
 #pragma unroll
                 for (int s2 = 0; s2 <= TB; ++s2) SU.ghost_s[s2] = p.ghost[(pd.parity0 + s2) & 1];
                 SU.dst_final = pd.dst_final;
                 SU.dst_penult = pd.dst_penult;
-                SU.u = u;
-                SU.q = q;
             }
         }
         const int n_it = (ug.zb - ug.za) + 2 * H;
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(NT, MINB)
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
                 if (!(plane_ghost || any_ghost_col)) continue;
                 const double* ghost =
-                    (CHAIN ? SU.ghost_s[s] : p.ghost[(p.parity0 + s) & 1]) + (long long)k * p.plane;
+                    (CHAIN ? SU2[seq & 1].ghost_s[s] : p.ghost[(p.parity0 + s) & 1]) + (long long)k * p.plane;
                 const uint32_t fix = plane_ghost ? ok_mask : col_fix;
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
@@ -861,16 +861,16 @@ __global__ void __launch_bounds__(NT, MINB)
                         if ((out_mask >> (2 * i + 1)) & 1) stg[sidx[i] + 1] = val[i].y;
                     }
                     if (any_odd_col && k >= p.zout_lo && k < p.zout_hi) {
-                        double* dst = (CHAIN ? SU.dst_final : p.dst_final) + (long long)k * p.plane;
+                        double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
                             if ((odd_mask >> (2 * i)) & 1) dst[colidx[2 * i]] = val[i].x;
                             if ((odd_mask >> (2 * i + 1)) & 1) dst[colidx[2 * i + 1]] = val[i].y;
                         }
                     }
-                    if (CHAIN ? SU.dst_penult != nullptr : has_penult_1) {  // final pass only:
+                    if (CHAIN ? (uflags & 1) != 0 : has_penult_1) {  // final pass only:
                         // level TB-1 of the same cells
-                        double* pen = (CHAIN ? SU.dst_penult : p.dst_penult) + (long long)k * p.plane;
+                        double* pen = (CHAIN ? SU2[seq & 1].dst_penult : p.dst_penult) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
                             const double2 c2 = zq[TB - 1][i][R];  // level TB-1 at plane k
@@ -925,11 +925,11 @@ __global__ void __launch_bounds__(NT, MINB)
                     pend_y = ug.ty * OY;
                     pend_z = j - H - p.oz0;
                     pend_b = int(g % 3);
-                    if constexpr (CHAIN) pend_q = SU.q;
+                    if constexpr (CHAIN) pend_q = uflags >> 1;
                 }
             }
             if constexpr (CHAIN)
-                if (tid == STORE_TID && it == n_it - 1) pub_next = SU.u;  // unit finished
+                if (tid == STORE_TID && it == n_it - 1) pub_next = u;  // unit finished
             // three staging planes: the plane the next iteration writes was handed to the store
             // issued two iterations ago, so only that older store must have finished reading
             if (tid == STORE_TID) {

@@ -108,7 +108,7 @@ class GpuConfig:
     graphs: int = 0
     emulate_slabs: int = 0  # >1: that many z-slabs on ONE device (decomposition tests)
     chain: int = 0       # 1: chain same-depth passes into one dependency-driven launch; -1: off;
-                         # 0: auto (grids of at most 2^22 cells)
+                         # 0: auto (grids <= 256^3 cells, not var7pt)
 
     def to_c(self) -> GirihGpuConfig:
         return GirihGpuConfig(self.tb, self.variant, self.zchunks, self.ngpus, 1, self.device,
