@@ -148,6 +148,19 @@ const Variant* select_variant(int kind, int tb, int requested) {
     throw_err(GIRIH_EINVAL, "no compiled kernel variant for the requested fused step count");
 }
 
+// Default variant of a chained launch: the chained var7pt TB=2 kernel spills at the 448-thread
+// CTA's 128-register cap, so chains take the 224-thread 64x16 tile (254 registers, no spill):
+// 128^3 72 K vs 59 K MLUP/s one launch per pass, 64^3 24 K vs 18 K.
+const Variant* select_chain_variant(int kind, int tb, int requested) {
+    if (requested < 0 && kind == K_VAR7 && tb == 2) {
+        int n;
+        const Variant* t = variant_table(kind, &n);
+        for (int i = 0; i < n; ++i)
+            if (t[i].tb == 2 && t[i].lx == 64 && t[i].ly == 16 && t[i].threads == 224) return &t[i];
+    }
+    return select_variant(kind, tb, requested);
+}
+
 inline int parity_of(long long t) { return int(((t % 2) + 2) % 2); }
 
 // ------------------------------------------------------------------------------------------
@@ -1088,15 +1101,15 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     }
     // pass chaining (single-slab handles): per-(pass, z chunk) tile counters, allocated
     // before any graph capture
-    // auto (chain = 0): grids of at most 256^3 cells, except var7pt. A chained launch removes
+    // auto (chain = 0): grids of at most 256^3 cells (var7pt: 128^3). A chained launch removes
     // the per-pass ramp-up and tail (~20 us per pass) and allows long z chunks (fewer re-read
     // halo planes), but its kernel carries the dependency and publication state: it wins up
-    // to 256^3 (const7pt +13%, var25pt 128^3 +38%) and loses at 512^3 (-3..-9%). The chained
-    // var7pt kernel spills at the 448-thread CTA's 128-register cap and always loses (DESIGN.md
-    // section 4b).
+    // to 256^3 (const7pt +13%, var25pt 128^3 +38%) and loses at 512^3 (-3..-9%). var7pt chains
+    // run a smaller CTA (select_chain_variant) that wins to 128^3 only.
     const long long cells = (long long)h.nx * h.ny * h.nz;
     const bool want_chain =
-        h.cfg.chain > 0 || (h.cfg.chain == 0 && cells <= (1ll << 24) && h.kind != K_VAR7);
+        h.cfg.chain > 0 ||
+        (h.cfg.chain == 0 && cells <= (h.kind == K_VAR7 ? (1ll << 21) : (1ll << 24)));
     const bool can_chain = want_chain && h.slabs.size() == 1 && h.nranks == 1 &&
                            !std::getenv("GIRIH_TRACE") && !std::getenv("GIRIH_NO_CHAIN");
     if (can_chain) {
@@ -1178,6 +1191,9 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         st.variant = global_index_of(var);
         st.tb_used = std::max(st.tb_used, ps.tb);
         if (can_chain) {
+            const Variant* cvar = select_chain_variant(
+                h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
+            if (cvar->tb != ps.tb) cvar = select_chain_variant(h.kind, ps.tb, -1);
             // the longest run of passes with this depth (same variant and tile grid) that fits
             // one launch: <= CHAIN_MAX passes, <= CHAIN_DESC distinct buffer sets
             std::vector<std::array<int, 5>> keys;
@@ -1199,7 +1215,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             }
             Slab& s = h.slabs[0];
             LaunchInfo li;
-            PassParams p = build_params(h, ps, var, 0, t, &li, -1, -1, true);
+            PassParams p = build_params(h, ps, cvar, 0, t, &li, -1, -1, true);
             // a unit reads z chunks +-1 of the previous pass only if its halo fits in a chunk
             if (e - pidx >= 2 && ps.tb * h.R <= p.zc_len) {
                 const int npass = int(e - pidx);
@@ -1213,11 +1229,11 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                     while (idx[f - pidx] != int(k)) tk += plan[f++].tb;
                     const Pass& pf = plan[f];
                     PassDesc& d = cd.d[k];
-                    d.vmap = tensor_map(h, 0, s.buf[pf.src]->p, 1, var->lx, var->ly);
+                    d.vmap = tensor_map(h, 0, s.buf[pf.src]->p, 1, cvar->lx, cvar->ly);
                     d.umap = pf.src_prev >= 0 ? tensor_map(h, 0, s.buf[pf.src_prev]->p, 1,
-                                                           var->aux_x, var->aux_y)
+                                                           cvar->aux_x, cvar->aux_y)
                                               : d.vmap;
-                    d.omap = tensor_map(h, 0, s.buf[pf.dst]->p, 1, p.ox, var->ly - 2 * pf.tb * h.R, 1);
+                    d.omap = tensor_map(h, 0, s.buf[pf.dst]->p, 1, p.ox, cvar->ly - 2 * pf.tb * h.R, 1);
                     d.dst_final = s.buf[pf.dst]->p;
                     d.dst_penult = pf.dst_penult >= 0 ? s.buf[pf.dst_penult]->p : nullptr;
                     d.parity0 = parity_of(tk);
@@ -1230,15 +1246,16 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 work_base[0] += (long long)npass * p.units;
                 const CUtensorMap& cmap =
                     h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc,
-                                          var->aux_x, var->aux_y)
+                                          cvar->aux_x, cvar->aux_y)
                              : cd.d[0].vmap;
                 const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
                 if (time_passes) GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
-                GCHECK(var->launch_chain(cmap, cd, p, li.grid, s.stream));
+                GCHECK(cvar->launch_chain(cmap, cd, p, li.grid, s.stream));
                 if (time_passes) GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
                 st.computed += li.computed_lups * npass;
                 st.grid = li.grid;
                 st.zchunks = li.zchunks;
+                st.variant = global_index_of(cvar);
                 st.n_launches++;
                 st.n_passes += npass;
                 for (int q = 0; q < npass; ++q) t += plan[pidx + q].tb;
