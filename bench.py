@@ -249,9 +249,12 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     lups = cells * world * T * args.steps
     value = lups / kernel_s / 1e6
     launches = sum(r.n_launches for r in reps)
+    passes = sum(r.n_passes for r in reps)
     pass_s = sum(r.pass_seconds for r in reps)
     avg_launch = pass_s / max(1, launches)
-    achieved = cells * B1[kind] / avg_launch / 1e9  # algorithmic bytes per launch / duration
+    passes_per_launch = passes / max(1, launches)  # > 1 for chained launches (small grids)
+    # algorithmic bytes per launch / its CUDA-event duration
+    achieved = cells * B1[kind] * passes_per_launch / avg_launch / 1e9
     traffic, traffic_src = ncu_traffic(kind, n)
     r0 = reps[-1]
     ds.close()
@@ -306,7 +309,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         "config": {"workload": f"BASELINE configs[1]: {KINDS[kind]} {n}^3 interior, T={T}, "
                                f"seed 42", "stencil": KINDS[kind], "n": n, "time_steps": T,
                    "tb": r0.tb_used, "variant": r0.variant_used, "zchunks": r0.zchunks_used,
-                   "grid_ctas": r0.grid_ctas, "passes_per_step": r0.n_launches,
+                   "grid_ctas": r0.grid_ctas, "passes_per_step": r0.n_passes,
+                   "launches_per_step": r0.n_launches,
                    "l2": f"inputs {cells * 8 * (2 + (7 if kind == 1 else 13 if kind == 3 else kind // 2)) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
                    "global_grid": [n, n, n * world],
                    "parallelism": (f"z-slabs x{world} (NCCL halo exchange of R*TB planes per pass)"
@@ -316,7 +320,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": hbm_src, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": cells * B1[kind],
+                     "algorithmic_bytes_per_launch": cells * B1[kind] * passes_per_launch,
                      "avg_launch_ms": avg_launch * 1e3,
                      "lup_roofline_mlups": hbm * 1e9 * r0.tb_used / B1[kind] / 1e6,
                      "frac_of_lup_roofline": value / (hbm * 1e9 * r0.tb_used / B1[kind] / 1e6),

@@ -35,8 +35,9 @@ for kind in [int(k) for k in a.kinds.split(",")]:
                 r = ds.step(nt)
                 tb = r.tb_used
                 rec = {"kind": g.KINDS[kind], "n": n, "nt": nt, "tb": tb, "mlups": round(r.mlups),
-                       "kernel_s": round(r.kernel_seconds, 5), "passes": r.n_launches,
-                       "eff_GBs": round(n ** 3 * B1[kind] * r.n_launches / r.pass_seconds / 1e9, 1),
+                       "kernel_s": round(r.kernel_seconds, 5), "passes": r.n_passes,
+                       "launches": r.n_launches, "zchunks": r.zchunks_used,
+                       "eff_GBs": round(n ** 3 * B1[kind] * r.n_passes / r.pass_seconds / 1e9, 1),
                        "frac_hbm_roof_tb": round(r.mlups / (HBM * 1e3 * tb / B1[kind]), 3),
                        "frac_hbm_roof_tb1": round(r.mlups / (HBM * 1e3 / B1[kind]), 3)}
         except g.GirihError as e:
