@@ -43,6 +43,10 @@
 #include <cuda.h>
 #include <cstdint>
 
+#ifndef GIRIH_XSHFL
+#define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
+#endif
+
 namespace girih_gpu {
 
 enum { K_CONST7 = 0, K_VAR7 = 1, K_CONST25 = 2, K_VAR25 = 3 };
@@ -371,6 +375,10 @@ __global__ void __launch_bounds__(NT, MINB)
     constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA, OY = CFG::OY;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr bool CQ = CFG::CQ;
+    // x neighbours by warp shuffle (misaligned pair loads cost two shared-memory wavefronts
+    // per quarter warp). Measured (same box): const7pt single-pass +4.5% (512^3); const7pt
+    // chained -15%, var7pt -2%, const25pt -5% (radius 4: 16 shuffles per pair), var25pt +-0.
+    constexpr bool XSHFL = GIRIH_XSHFL && KIND == K_CONST7 && !CHAIN;
     constexpr int AX = CFG::AX, AYX = CFG::AYX, AUXPLANE = CFG::AUXPLANE;
     constexpr int GUARD = CFG::GUARD, STAGE = CFG::STAGE;
     constexpr uint32_t PLANE_BYTES = CELLS * sizeof(double);
@@ -721,15 +729,30 @@ __global__ void __launch_bounds__(NT, MINB)
                         continue;
                     }
                     const int h2 = lcell[i] >> 1;  // pair index within a plane
-                    // x neighbourhood x = c-XA .. c+1+XA from XA+1 aligned pair loads
+                    // x neighbourhood x = c-XA .. c+1+XA: XA+1 aligned pair loads, or (XSHFL)
+                    // the centre pair and warp shuffles, since the lanes of a warp own
+                    // consecutive pairs of a tile row. Edge lanes get values from beyond the
+                    // row, exactly as the shifted loads did: those cells are never output.
                     double xs[2 * XA + 2];
+                    if constexpr (XSHFL) {
+                        const double2 ctr = CFG::STACK ? colw[CFG::STACK ? i + R : 0] : pc[h2];
+                        const int lane = tid & 31;
 #pragma unroll
-                    for (int t = 0; t <= XA; ++t) {
-                        const double2 w = (CFG::STACK && t == XA / 2)
-                                              ? colw[CFG::STACK ? i + R : 0]
-                                              : pc[h2 - XA / 2 + t];
-                        xs[2 * t] = w.x;
-                        xs[2 * t + 1] = w.y;
+                        for (int t = 0; t <= XA; ++t) {
+                            const int d = t - XA / 2;
+                            xs[2 * t] = d == 0 ? ctr.x : __shfl_sync(0xffffffffu, ctr.x, lane + d);
+                            xs[2 * t + 1] =
+                                d == 0 ? ctr.y : __shfl_sync(0xffffffffu, ctr.y, lane + d);
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t <= XA; ++t) {
+                            const double2 w = (CFG::STACK && t == XA / 2)
+                                                  ? colw[CFG::STACK ? i + R : 0]
+                                                  : pc[h2 - XA / 2 + t];
+                            xs[2 * t] = w.x;
+                            xs[2 * t + 1] = w.y;
+                        }
                     }
                     auto X = [&](int q, int dx) -> double { return xs[q + dx + XA]; };
                     auto Yp = [&](int dy) -> double2 {
