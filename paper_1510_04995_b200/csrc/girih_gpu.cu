@@ -506,6 +506,9 @@ struct Handle {
     bool uploads_all = false;  // girih_gpu_run: u, v and coefficients are uploaded before use
     std::vector<Slab> slabs;
     bool emulated = false;  // several slabs on one device
+    // single-process slabs: passes store their boundary planes straight into the neighbours'
+    // halos (PassParams::push_*), replacing the exchange copies
+    bool push_peers = false;
     // multi-process mode: this process owns slab `rank` of `nranks`; halos move over NCCL
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
@@ -706,6 +709,15 @@ void setup_slabs(Handle& h) {
                 cudaGetLastError();
             }
         }
+    }
+    // halo push needs peer access between every adjacent pair (always true when emulated)
+    h.push_peers = nslab > 1 && !dist && !std::getenv("GIRIH_NO_PUSH");
+    for (int g = 0; h.push_peers && !h.emulated && g + 1 < nslab; ++g) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, h.slabs[g].device, h.slabs[g + 1].device);
+        int ok2 = 0;
+        cudaDeviceCanAccessPeer(&ok2, h.slabs[g + 1].device, h.slabs[g].device);
+        if (!ok || !ok2) h.push_peers = false;
     }
     GCHECK(cudaSetDevice(h.slabs[0].device));
     GCHECK(cudaDeviceGetAttribute(&h.sm_count, cudaDevAttrMultiProcessorCount, h.slabs[0].device));
@@ -1031,6 +1043,22 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         GCHECK(cudaMemsetAsync(s.trace->p, 0, 4096 * 8 * 8, s.stream));
         p.trace = reinterpret_cast<unsigned long long*>(s.trace->p);
     }
+    if (h.push_peers && zlo == s.zout_lo && zhi == s.zout_hi) {
+        const long long plane = (long long)h.pitch * h.Y;
+        if (slab_index > 0) {
+            const Slab& n = h.slabs[slab_index - 1];
+            p.push_dn_final = n.buf[ps.dst]->p;
+            p.push_dn_penult = ps.dst_penult >= 0 ? n.buf[ps.dst_penult]->p : nullptr;
+            p.push_dn_off = (long long)(s.zoff - n.zoff) * plane;
+        }
+        if (slab_index + 1 < int(h.slabs.size())) {
+            const Slab& n = h.slabs[slab_index + 1];
+            p.push_up_final = n.buf[ps.dst]->p;
+            p.push_up_penult = ps.dst_penult >= 0 ? n.buf[ps.dst_penult]->p : nullptr;
+            p.push_up_off = (long long)(s.zoff - n.zoff) * plane;
+        }
+        p.push_hz = h.hz;
+    }
     li->grid = std::min(p.units, max_grid);
     li->zchunks = p.nzc;
     li->computed_lups = tg.computed_lups;
@@ -1090,6 +1118,24 @@ void exchange_halos(Handle& h, int buf) {
     }
 }
 
+// Halo push: a slab's next pass reads halo planes its neighbours pushed during this pass, and
+// overwrites buffers its neighbours may still be reading: each slab's stream waits for both
+// neighbours' passes. (Emulated slabs share one stream, which already orders them.)
+void order_slabs(Handle& h) {
+    const int ns = int(h.slabs.size());
+    if (h.emulated || ns < 2) return;
+    for (int g = 0; g < ns; ++g) {
+        GCHECK(cudaSetDevice(h.slabs[g].device));
+        GCHECK(cudaEventRecord(h.slabs[g].done, h.slabs[g].stream));
+    }
+    for (int g = 0; g < ns; ++g) {
+        Slab& s = h.slabs[g];
+        GCHECK(cudaSetDevice(s.device));
+        if (g > 0) GCHECK(cudaStreamWaitEvent(s.stream, h.slabs[g - 1].done, 0));
+        if (g + 1 < ns) GCHECK(cudaStreamWaitEvent(s.stream, h.slabs[g + 1].done, 0));
+    }
+}
+
 StepStats do_step(Handle& h, long long steps, bool time_passes) {
     StepStats st;
     if (steps == 0) return st;
@@ -1098,6 +1144,11 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     for (const Pass& ps : plan) {
         for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
             if (b >= 2) ensure_scratch(h, b & 1);
+        // a slab supplies its neighbours' whole halo from its own planes
+        if (h.slabs.size() > 1 || h.nranks > 1)
+            for (const Slab& s : h.slabs)
+                if (s.zout_hi - s.zout_lo < ps.tb * h.R)
+                    throw_err(GIRIH_EINVAL, "z-slab thinner than the fused-step halo (TB*R planes)");
     }
     // pass chaining (single-slab handles): per-(pass, z chunk) tile counters, allocated
     // before any graph capture
@@ -1307,8 +1358,11 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             st.zchunks = li.zchunks;
             st.n_launches++;
         }
-        // halo exchange of the levels the next pass reads
-        if (h.slabs.size() > 1 || h.nranks > 1) {
+        // halo exchange of the levels the next pass reads: pushed by the pass itself
+        // (single-process slabs; the next pass only waits for its neighbours), or copied
+        if (h.push_peers) {
+            order_slabs(h);
+        } else if (h.slabs.size() > 1 || h.nranks > 1) {
             exchange_halos(h, ps.dst);
             if (h.kind == K_CONST25 && ps.dst_penult >= 0) exchange_halos(h, ps.dst_penult);
         }

@@ -84,6 +84,16 @@ struct PassParams {
     unsigned long long* trace;  // optional per-iteration phase clocks of CTA 0 (debug)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
                              // innermost box coordinate 16-byte aligned (even for fp64)
+    // Halo push (single-process z-slabs): the output cells of this slab's bottom / top push_hz
+    // own planes are also stored straight into the lower / upper neighbour's halo planes (peer
+    // memory over NVLink, or the same device for emulated slabs), so no exchange step follows
+    // the pass. A neighbour cell = its base + (local plane k * plane + push_*_off) + column.
+    double* push_dn_final;
+    double* push_up_final;
+    double* push_dn_penult;
+    double* push_up_penult;
+    long long push_dn_off, push_up_off;
+    int push_hz;
 };
 
 // Pass chaining. One launch may run a sequence of passes over the same tile grid. Units are
@@ -901,6 +911,33 @@ __global__ void __launch_bounds__(NT, MINB)
                             if ((out_mask >> b) & 1 && !((ghost_mask >> b) & 1)) pen[colidx[b]] = c2.x;
                             if ((out_mask >> (b + 1)) & 1 && !((ghost_mask >> (b + 1)) & 1))
                                 pen[colidx[b + 1]] = c2.y;
+                        }
+                    }
+                    if constexpr (!CHAIN) {
+                        // halo push: boundary planes go to the neighbour slab as they are made
+                        const bool dn = p.push_dn_final && k < p.zout_lo + p.push_hz;
+                        const bool up = p.push_up_final && k >= p.zout_hi - p.push_hz;
+                        // (a thin slab's plane may belong to both neighbours' halos)
+#pragma unroll
+                        for (int side = 0; side < 2; ++side) {
+                            if (!(side ? up : dn)) continue;
+                            const long long o =
+                                (long long)k * p.plane + (side ? p.push_up_off : p.push_dn_off);
+                            double* fin = (side ? p.push_up_final : p.push_dn_final) + o;
+                            double* pen = has_penult_1
+                                              ? (side ? p.push_up_penult : p.push_dn_penult) + o
+                                              : nullptr;
+#pragma unroll
+                            for (int i = 0; i < PPT; ++i) {
+                                const double2 c2 = zq[TB - 1][i][R];
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) {
+                                    const int b = 2 * i + q;
+                                    if (!((out_mask >> b) & 1) || ((ghost_mask >> b) & 1)) continue;
+                                    fin[colidx[b]] = q ? val[i].y : val[i].x;
+                                    if (pen) pen[colidx[b]] = q ? c2.y : c2.x;
+                                }
+                            }
                         }
                     }
                     staged = true;
