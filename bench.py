@@ -203,21 +203,44 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     hbm, hbm_src = measured_peaks()
     cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant)
     dist = None
+    halo = None
     if world > 1:
-        # weak scaling: a 512 x 512 x (512 N) grid in z-slabs, one slab per rank/GPU, R*TB halos
-        # exchanged over NCCL after every pass (inside the library); torch.distributed is the
-        # plumbing for the NCCL id and the max-over-ranks timing
+        # weak scaling: a 512 x 512 x (512 N) grid in z-slabs, one slab per rank/GPU. Halos of
+        # R*TB planes: pushed by each pass straight into the neighbour GPUs' memory (CUDA IPC
+        # over NVLink, passes ordered by stream memory operations), or exchanged over NCCL after
+        # every pass (--halo nccl, and the fallback if IPC is unavailable). torch.distributed is
+        # the plumbing for the IPC blobs / NCCL id and the max-over-ranks timing.
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(dev)
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(g.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
-        ds = g.DeviceState.slab_seeded(kind, g.GridSpec(n, n, n * world), 42, True, rank, world,
-                                       nid, cfg)
+        ggrid = g.GridSpec(n, n, n * world)
+        ds = None
+        if args.halo == "push":
+            try:
+                ds = g.DeviceState.slab_seeded(kind, ggrid, 42, True, rank, world, None, cfg)
+                blobs = [None] * world
+                dist.all_gather_object(blobs, ds.ipc_export())
+                ds.ipc_connect(blobs[rank - 1] if rank > 0 else None,
+                               blobs[rank + 1] if rank + 1 < world else None)
+                ok = torch.ones(1, device="cuda")
+            except g.GirihError as e:
+                print(f"rank {rank}: IPC halo push unavailable ({e}); using NCCL", file=sys.stderr)
+                ok = torch.zeros(1, device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() < 1 and ds is not None:  # every rank falls back together
+                ds.close()
+                ds = None
+            dist.barrier()
+            halo = "push" if ds is not None else None
+        if ds is None:
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(g.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nid = bytes(idt.cpu().numpy().tobytes())
+            ds = g.DeviceState.slab_seeded(kind, ggrid, 42, True, rank, world, nid, cfg)
+            halo = "nccl"
     else:
         ds = g.DeviceState.seeded(kind, g.GridSpec(n, n, n), 42, remap=True, config=cfg)
     tuned = None
@@ -313,7 +336,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                    "launches_per_step": r0.n_launches,
                    "l2": f"inputs {cells * 8 * (2 + (7 if kind == 1 else 13 if kind == 3 else kind // 2)) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
                    "global_grid": [n, n, n * world],
-                   "parallelism": (f"z-slabs x{world} (NCCL halo exchange of R*TB planes per pass)"
+                   "parallelism": ((f"z-slabs x{world} (halos of R*TB planes pushed by each pass "
+                                    f"into the neighbours' memory over NVLink, CUDA IPC)"
+                                    if halo == "push" else
+                                    f"z-slabs x{world} (NCCL halo exchange of R*TB planes per pass)")
                                    if world > 1 else "single GPU"),
                    "tuned": tuned},
         "gpu_launches": launches,
@@ -349,6 +375,9 @@ def main():
     ap.add_argument("--tb", type=int, default=0)
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--zchunks", type=int, default=0)
+    ap.add_argument("--halo", default="push", choices=["push", "nccl"],
+                    help="N > 1: passes push halos into the neighbours' memory (CUDA IPC) or "
+                         "exchange them over NCCL after every pass")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)

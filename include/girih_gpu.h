@@ -131,6 +131,16 @@ int girih_gpu_open_slab_seeded(int kind, int nx, int ny, int nz, int pad_x, unsi
                                int remap, int rank, int nranks, const unsigned char* nccl_id,
                                const girih_gpu_config* cfg, void** handle);
 
+/* Multi-process halo push over CUDA IPC (open the slab with nccl_id = NULL): each rank exports
+ * its buffers and pass flags, passes the blob to its z neighbours (any host transport), then
+ * connects to them (NULL for a missing neighbour) and barriers with all ranks. From then on a
+ * pass stores its boundary planes straight into the neighbours' halos (peer memory over NVLink)
+ * and the ranks order their passes with stream memory operations on each other's flags; no
+ * NCCL, no exchange step. */
+#define GIRIH_GPU_IPC_BYTES 512
+int girih_gpu_ipc_export(void* handle, unsigned char* out, int len);
+int girih_gpu_ipc_connect(void* handle, const unsigned char* lower, const unsigned char* upper);
+
 /* Re-upload u, v, coefficients, cc and t_current from a host view of the same shape. */
 int girih_gpu_upload(void* handle, const girih_state_view* state);
 

@@ -20,6 +20,9 @@ GIRIH_ENOMEM = -4
 GIRIH_ESTATE = -5
 
 
+GIRIH_GPU_IPC_BYTES = 512  # include/girih_gpu.h
+
+
 class GirihStateView(C.Structure):
     _fields_ = [
         ("kind", C.c_int),
@@ -86,6 +89,8 @@ SIGNATURES = {
     "girih_gpu_open_slab_seeded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.c_ulonglong, C.c_int, C.c_int, C.c_int, C.c_char_p,
                                              C.POINTER(GirihGpuConfig), C.POINTER(C.c_void_p)]),
+    "girih_gpu_ipc_export": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
+    "girih_gpu_ipc_connect": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
     "girih_gpu_upload": (C.c_int, [C.c_void_p, C.POINTER(GirihStateView)]),
     "girih_gpu_step": (C.c_int, [C.c_void_p, C.c_longlong, C.POINTER(GirihGpuReport)]),
     "girih_gpu_download": (C.c_int, [C.c_void_p, C.POINTER(GirihStateView)]),

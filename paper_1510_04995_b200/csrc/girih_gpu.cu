@@ -512,6 +512,17 @@ struct Handle {
     // multi-process mode: this process owns slab `rank` of `nranks`; halos move over NCCL
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
+    // multi-process halo push (girih_gpu_ipc_export / _connect): the neighbour ranks' buffers
+    // and pass flags mapped through CUDA IPC; side 0 = rank-1 (lower), 1 = rank+1 (upper)
+    bool ipc = false;
+    struct Peer {
+        double* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+        int* flags = nullptr;  // the neighbour's flags[2] (we write the entry for our side)
+        int zoff = 0;
+        bool open = false;
+    } peer[2];
+    std::unique_ptr<DevBuf> ipc_flags;  // ours: [0] = passes done by rank-1, [1] = by rank+1
+    unsigned epoch = 0;                 // passes this rank has launched
     int sm_count = 0;
     // timing events (slab 0 stream)
     std::vector<cudaEvent_t> ev;
@@ -1043,6 +1054,19 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         GCHECK(cudaMemsetAsync(s.trace->p, 0, 4096 * 8 * 8, s.stream));
         p.trace = reinterpret_cast<unsigned long long*>(s.trace->p);
     }
+    if (h.ipc && zlo == s.zout_lo && zhi == s.zout_hi) {
+        const long long plane = (long long)h.pitch * h.Y;
+        for (int side = 0; side < 2; ++side) {
+            const Handle::Peer& n = h.peer[side];
+            if (!n.open) continue;
+            double*& fin = side ? p.push_up_final : p.push_dn_final;
+            double*& pen = side ? p.push_up_penult : p.push_dn_penult;
+            fin = n.buf[ps.dst];
+            pen = ps.dst_penult >= 0 ? n.buf[ps.dst_penult] : nullptr;
+            (side ? p.push_up_off : p.push_dn_off) = (long long)(s.zoff - n.zoff) * plane;
+        }
+        p.push_hz = h.hz;
+    }
     if (h.push_peers && zlo == s.zout_lo && zhi == s.zout_hi) {
         const long long plane = (long long)h.pitch * h.Y;
         if (slab_index > 0) {
@@ -1115,6 +1139,47 @@ void exchange_halos(Handle& h, int buf) {
                                        n.buf[buf]->p + (size_t)n.zout_lo * pe, n.device,
                                        (size_t)hz * pe * 8, s.stream));
         }
+    }
+}
+
+// Stream memory operations (driver API, resolved at run time like cuTensorMapEncodeTiled)
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    GCHECK(cudaGetDriverEntryPointByVersion(name, &q, 11070, cudaEnableDefault, &r));
+    if (r != cudaDriverEntryPointSuccess || !q)
+        throw_err(GIRIH_ECUDA, std::string(name) + " entry point unavailable");
+    return reinterpret_cast<StreamValueFn>(q);
+}
+
+// Multi-process halo push. Before pass `epoch`, wait (on the GPU front end, no kernel spins)
+// until both neighbours have finished pass epoch-1: they pushed the halo planes this pass reads
+// and have stopped reading the buffers it pushes into. After the pass, tell both neighbours
+// (the write is fenced after the pass's peer stores).
+void ipc_before_pass(Handle& h) {
+    static StreamValueFn wait = stream_value_fn("cuStreamWaitValue32");
+    Slab& s = h.slabs[0];
+    for (int side = 0; side < 2; ++side) {
+        if (!h.peer[side].open) continue;
+        const CUresult r = wait(reinterpret_cast<CUstream>(s.stream),
+                                reinterpret_cast<CUdeviceptr>(
+                                    reinterpret_cast<int*>(h.ipc_flags->p) + side),
+                                h.epoch, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) throw_err(GIRIH_ECUDA, "cuStreamWaitValue32 failed");
+    }
+}
+void ipc_after_pass(Handle& h) {
+    static StreamValueFn write = stream_value_fn("cuStreamWriteValue32");
+    Slab& s = h.slabs[0];
+    ++h.epoch;
+    for (int side = 0; side < 2; ++side) {
+        if (!h.peer[side].open) continue;
+        // our pass count goes into the neighbour's entry for the side we are on
+        const CUresult r = write(reinterpret_cast<CUstream>(s.stream),
+                                 reinterpret_cast<CUdeviceptr>(h.peer[side].flags + (1 - side)),
+                                 h.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) throw_err(GIRIH_ECUDA, "cuStreamWriteValue32 failed");
     }
 }
 
@@ -1335,6 +1400,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                                                  var->ly - 2 * ps.tb * h.R, 1);
             // inside a stream capture a plain record only orders streams: record as graph nodes
             const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+            if (h.ipc) ipc_before_pass(h);
             if (time_passes && g == 0)
                 GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
             GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
@@ -1360,7 +1426,9 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         }
         // halo exchange of the levels the next pass reads: pushed by the pass itself
         // (single-process slabs; the next pass only waits for its neighbours), or copied
-        if (h.push_peers) {
+        if (h.ipc) {
+            ipc_after_pass(h);
+        } else if (h.push_peers) {
             order_slabs(h);
         } else if (h.slabs.size() > 1 || h.nranks > 1) {
             exchange_halos(h, ps.dst);
@@ -1422,6 +1490,17 @@ void destroy(Handle* h) {
     if (h->comm) {
         nccl().commDestroy(h->comm);
         h->comm = nullptr;
+    }
+    if (h->ipc && !h->slabs.empty()) {
+        cudaSetDevice(h->slabs[0].device);
+        cudaStreamSynchronize(h->slabs[0].stream);
+        for (auto& n : h->peer) {
+            if (!n.open) continue;
+            for (double* b : n.buf) cudaIpcCloseMemHandle(b);
+            cudaIpcCloseMemHandle(n.flags);
+            n.open = false;
+        }
+        cudaGetLastError();
     }
     for (Slab& s : h->slabs) {
         cudaSetDevice(s.device);
@@ -1925,7 +2004,7 @@ int girih_gpu_open_slab_seeded(int kind, int nx, int ny, int nz, int pad_x, unsi
                                const girih_gpu_config* cfg, void** handle) {
     Handle* h = nullptr;
     const int rc = guarded([&] {
-        if (!handle || !nccl_id) throw_err(GIRIH_EINVAL, "null argument");
+        if (!handle) throw_err(GIRIH_EINVAL, "null argument");
         if (nranks < 1 || rank < 0 || rank >= nranks) throw_err(GIRIH_EINVAL, "bad rank");
         h = new Handle();
         h->cfg = cfg ? *cfg : default_config();
@@ -1936,17 +2015,88 @@ int girih_gpu_open_slab_seeded(int kind, int nx, int ny, int nz, int pad_x, unsi
         setup_geometry(*h, kind, nx, ny, nz, pad_x);
         validate_config(h->cfg, h->kind);
         setup_slabs(*h);
-        if (nranks > 1) {
+        if (nranks > 1 && nccl_id) {
             GCHECK(cudaSetDevice(h->slabs[0].device));
             ncclUniqueId u;
             std::memcpy(&u, nccl_id, sizeof u);
             NCHECK(nccl().commInitRank(&h->comm, nranks, u, rank));
+        } else if (nranks > 1) {  // halo push through CUDA IPC (girih_gpu_ipc_export/_connect)
+            h->ipc = true;
+            alloc_buf(h->ipc_flags, h->slabs[0].device, 1, h->slabs[0].stream);  // 2 ints, zeroed
         }
         init_state_device(*h, seed, remap);
+        if (h->ipc) {  // every buffer a neighbour may push into exists before it is exported
+            ensure_scratch(*h, 0);
+            ensure_scratch(*h, 1);
+        }
         *handle = h;
     });
     if (rc != GIRIH_OK && h) destroy(h);
     return rc;
+}
+
+namespace {
+struct IpcBlob {
+    cudaIpcMemHandle_t mem[4];  // u, v, even scratch, odd scratch
+    cudaIpcMemHandle_t flags;
+    int zoff, pitch, Y, X, magic;
+};
+constexpr int kIpcMagic = 0x67697269;  // "giri"
+static_assert(sizeof(IpcBlob) <= GIRIH_GPU_IPC_BYTES, "IPC blob size");
+}  // namespace
+
+int girih_gpu_ipc_export(void* handle, unsigned char* out, int len) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!out || len < GIRIH_GPU_IPC_BYTES) throw_err(GIRIH_EINVAL, "IPC buffer too small");
+        if (!h.ipc) throw_err(GIRIH_ESTATE, "handle not opened for IPC halo push");
+        Slab& s = h.slabs[0];
+        GCHECK(cudaSetDevice(s.device));
+        IpcBlob b{};
+        for (int i = 0; i < 4; ++i) GCHECK(cudaIpcGetMemHandle(&b.mem[i], s.buf[i]->p));
+        GCHECK(cudaIpcGetMemHandle(&b.flags, h.ipc_flags->p));
+        b.zoff = s.zoff;
+        b.pitch = h.pitch;
+        b.Y = h.Y;
+        b.X = h.X;
+        b.magic = kIpcMagic;
+        std::memset(out, 0, size_t(len));
+        std::memcpy(out, &b, sizeof b);
+    });
+}
+
+int girih_gpu_ipc_connect(void* handle, const unsigned char* lower, const unsigned char* upper) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!h.ipc) throw_err(GIRIH_ESTATE, "handle not opened for IPC halo push");
+        if ((h.rank > 0) != (lower != nullptr) || (h.rank + 1 < h.nranks) != (upper != nullptr))
+            throw_err(GIRIH_EINVAL, "neighbour blobs do not match this rank's position");
+        Slab& s = h.slabs[0];
+        GCHECK(cudaSetDevice(s.device));
+        const unsigned char* blobs[2] = {lower, upper};
+        for (int side = 0; side < 2; ++side) {
+            if (!blobs[side]) continue;
+            IpcBlob b;
+            std::memcpy(&b, blobs[side], sizeof b);
+            if (b.magic != kIpcMagic || b.pitch != h.pitch || b.Y != h.Y || b.X != h.X)
+                throw_err(GIRIH_EINVAL, "neighbour IPC blob does not match this grid");
+            Handle::Peer& n = h.peer[side];
+            for (int i = 0; i < 4; ++i) {
+                void* q = nullptr;
+                GCHECK(cudaIpcOpenMemHandle(&q, b.mem[i], cudaIpcMemLazyEnablePeerAccess));
+                n.buf[i] = static_cast<double*>(q);
+            }
+            void* f = nullptr;
+            GCHECK(cudaIpcOpenMemHandle(&f, b.flags, cudaIpcMemLazyEnablePeerAccess));
+            n.flags = static_cast<int*>(f);
+            n.zoff = b.zoff;
+            n.open = true;
+        }
+        // the local state is fully initialised before any neighbour may push into it; the
+        // caller barriers across ranks after every rank's connect
+        GCHECK(cudaStreamSynchronize(s.stream));
+        GCHECK(cudaDeviceSynchronize());
+    });
 }
 
 int girih_gpu_upload(void* handle, const girih_state_view* state) {

@@ -293,17 +293,30 @@ class DeviceState:
 
     @classmethod
     def slab_seeded(cls, kind: int, grid: GridSpec, seed: int, remap: bool, rank: int, nranks: int,
-                    nccl_id: bytes, config: Optional[GpuConfig] = None) -> "DeviceState":
-        """This process's z-slab `rank` of `nranks` of the global grid (one process per GPU);
-        halos move over NCCL. `nccl_id` comes from nccl_unique_id() on rank 0."""
+                    nccl_id: Optional[bytes], config: Optional[GpuConfig] = None) -> "DeviceState":
+        """This process's z-slab `rank` of `nranks` of the global grid (one process per GPU).
+        With `nccl_id` (from nccl_unique_id() on rank 0) halos move over NCCL after every pass;
+        with None the passes push them into the neighbours' memory: call ipc_export(), hand the
+        blobs to the z neighbours, ipc_connect() and barrier before the first step."""
         config = config or GpuConfig()
         cfg = config.to_c()
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(bytes(nccl_id), max(len(nccl_id), 128))
+        idbuf = (C.create_string_buffer(bytes(nccl_id), max(len(nccl_id), 128))
+                 if nccl_id is not None else None)
         check(load().girih_gpu_open_slab_seeded(int(kind), grid.nx, grid.ny, grid.nz, grid.pad_x,
                                                 int(seed), int(bool(remap)), int(rank), int(nranks),
                                                 idbuf, C.byref(cfg), C.byref(h)))
         return cls(h, kind, grid, config)
+
+    def ipc_export(self) -> bytes:
+        """This slab's IPC blob (buffers + pass flags) for its z neighbours."""
+        buf = C.create_string_buffer(_lib.GIRIH_GPU_IPC_BYTES)
+        check(load().girih_gpu_ipc_export(self._handle(), buf, _lib.GIRIH_GPU_IPC_BYTES))
+        return buf.raw
+
+    def ipc_connect(self, lower: Optional[bytes], upper: Optional[bytes]) -> None:
+        """Map the z neighbours' blobs (None where there is no neighbour)."""
+        check(load().girih_gpu_ipc_connect(self._handle(), lower, upper))
 
     def _handle(self):
         if self._h is None or not self._h.value:

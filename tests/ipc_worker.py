@@ -1,0 +1,53 @@
+"""Worker for tests/test_gpu_parity.py::test_ipc_halo_push_two_processes (not a test module).
+
+One rank of a multi-process z-slab run whose halos move by the passes' own peer stores (CUDA
+IPC, no NCCL): gloo carries the IPC blobs, every rank checks its slab bitwise against a
+single-domain run of the same seeded grid. Launched by torch.distributed.run with two ranks."""
+import os
+import sys
+
+import torch.distributed as dist
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+import paper_1510_04995_b200 as g  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = int(os.environ.get("GIRIH_IPC_DEVICE", "0"))
+    bad = 0
+    for kind, (nx, ny, nz), steps in ((1, (40, 33, 50), 9), (3, (37, 30, 52), 5),
+                                      (2, (36, 29, 48), 6), (0, (41, 35, 47), 7)):
+        grid = g.GridSpec(nx, ny, nz, 0)
+        cfg = g.GpuConfig(device=dev)
+        with g.DeviceState.slab_seeded(kind, grid, 17, True, rank, world, None, cfg) as ds:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, ds.ipc_export())
+            if not os.environ.get("GIRIH_IPC_NEGATIVE"):  # (negative control: no halo traffic)
+                ds.ipc_connect(blobs[rank - 1] if rank > 0 else None,
+                               blobs[rank + 1] if rank + 1 < world else None)
+            dist.barrier()
+            ds.step(steps)
+            ds.step(steps + 1)  # a second call: odd start level, pass counters carry over
+            dist.barrier()
+            with g.DeviceState.seeded(kind, grid, 17, remap=True,
+                                      config=g.GpuConfig(device=dev, chain=-1)) as ref:
+                ref.step(steps)
+                ref.step(steps + 1)
+                host = ref.download(coeffs=False)
+            for f in ("u", "v"):
+                n, first = ds.compare(f, getattr(host, f))
+                if n:
+                    bad += 1
+                    print(f"rank {rank} {g.KINDS[kind]} field {f}: {n} cells differ, first {first}",
+                          flush=True)
+            dist.barrier()
+    print(f"rank {rank}: {'OK' if bad == 0 else 'FAIL'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -483,3 +483,19 @@ def test_chained_device_state_long_runs(girih, oracle):
         rc, rp = outs[1][2], outs[-1][2]
         assert rc.n_passes == rp.n_passes == 300
         assert rp.n_launches == 300 and rc.n_launches == 3  # 128 + 128 + 44
+
+
+def test_ipc_halo_push_two_processes(girih):
+    # multi-process z-slabs without NCCL: each pass stores its boundary planes straight into
+    # the neighbour rank's halo (CUDA IPC peer memory) and the ranks order their passes with
+    # stream memory operations on each other's flags. Two ranks share this GPU here: their
+    # kernels never wait on each other (only their streams do, on the front end), so the
+    # protocol is exercised exactly as on two GPUs. Bitwise against one domain, every kind.
+    import subprocess
+    import sys
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29571", os.path.join(HERE, "ipc_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert out.stdout.count(": OK") == 2, out.stdout[-3000:]
