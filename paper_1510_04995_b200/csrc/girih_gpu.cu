@@ -950,14 +950,14 @@ struct LaunchInfo {
 };
 
 // CTAs per SM of a variant (queried once per process and variant)
-int occupancy_of(const Variant* var) {
-    static std::map<const Variant*, int> cache;
-    auto it = cache.find(var);
+int occupancy_of(const Variant* var, bool chained = false) {
+    static std::map<std::pair<const Variant*, bool>, int> cache;
+    auto it = cache.find({var, chained});
     if (it != cache.end()) return it->second;
     int occ = 0;
-    GCHECK(var->occupancy(&occ));
+    GCHECK((chained ? var->occupancy_chain : var->occupancy)(&occ));
     if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
-    cache[var] = occ;
+    cache[{var, chained}] = occ;
     return occ;
 }
 
@@ -1015,7 +1015,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         zhi = s.zout_hi;
     }
     const int nzl = zhi - zlo;
-    const int max_grid = h.sm_count * occupancy_of(var);
+    const int max_grid = h.sm_count * occupancy_of(var, chained);
     const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid, chained);
     const int hx = tg.hx, OX = tg.ox;
     PassParams p{};
@@ -1359,7 +1359,8 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 cd.done = reinterpret_cast<int*>(s.chain_done->p);
                 GCHECK(cudaMemsetAsync(cd.done, 0, size_t(npass) * p.nzc * sizeof(int), s.stream));
                 p.work_base = int(work_base[0]);
-                work_base[0] += (long long)npass * p.units;
+                // every unit is drawn, plus one failing draw per CTA
+                work_base[0] += (long long)npass * p.units + li.grid;
                 const CUtensorMap& cmap =
                     h.nc > 0 ? tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc,
                                           cvar->aux_x, cvar->aux_y)

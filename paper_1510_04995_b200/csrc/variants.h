@@ -21,7 +21,8 @@ struct Variant {
     int aux_x0, aux_y0, aux_x, aux_y;  // coefficient (aux) box inside the tile
     LaunchFn launch;             // one pass
     LaunchChainFn launch_chain;  // cd.npass chained passes over the same tile grid
-    OccFn occupancy;
+    OccFn occupancy;             // resident CTAs per SM, single-pass kernel
+    OccFn occupancy_chain;       // the same for the chained kernel
 };
 
 // one table per kind, defined in variants_<kind>.cu
@@ -74,10 +75,10 @@ cudaError_t launch_zwave(const CUtensorMap& vmap, const CUtensorMap& cmap, const
     return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false>(cmap, cd, p, grid, stream);
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN = false>
 cudaError_t occupancy_zwave(int* blocks) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, false>;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN>;
     cudaError_t e =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
     if (e != cudaSuccess) return e;
@@ -93,7 +94,8 @@ cudaError_t occupancy_zwave(int* blocks) {
             ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AY,                                     \
             &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>,                                       \
             &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB>,                                 \
-            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>                                     \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>,                                    \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, true>                               \
     }
 
 }  // namespace girih_gpu

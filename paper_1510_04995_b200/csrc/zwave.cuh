@@ -43,6 +43,9 @@
 #include <cuda.h>
 #include <cstdint>
 
+#ifndef GIRIH_CHAIN_MINB_DROP
+#define GIRIH_CHAIN_MINB_DROP 0  // A/B: chained kernels one resident CTA fewer (more registers)
+#endif
 #ifndef GIRIH_XSHFL
 #define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
 #endif
@@ -264,7 +267,9 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, int 
             // latency hides behind a whole unit instead of stalling the producer warp
             next = *drawn;
             if (next < total) {
-                const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
+                // single-pass launches hand CTA b unit b first, so draws start at gridDim.x;
+                // chained ones draw every unit (a CTA that is not resident yet holds none)
+                const int d = (CHAIN ? 0 : int(gridDim.x)) + atomicAdd(p.work, 1) - p.work_base;
                 *drawn = d < total ? d : total;
             }
             uq[(c.seq + 1) % UQ] = next;
@@ -376,7 +381,7 @@ struct ZwaveConfig {
 // separate instantiations so that single-pass launches carry none of the chaining state (the
 // 128-register var7pt CTA spills otherwise, and shared-memory producer state cost 30%).
 template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN>
-__global__ void __launch_bounds__(NT, MINB)
+__global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 1) ? MINB - 1 : MINB)
     zwave_kernel(const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
                  const __grid_constant__ ChainDescs cd,     // per-pass buffers and maps
                  const __grid_constant__ PassParams p) {
@@ -487,11 +492,19 @@ __global__ void __launch_bounds__(NT, MINB)
     };
     static_assert(P >= PA, "the V producer draws units and must lead the aux producer");
     if (tid == 0) {
-        // the first unit is blockIdx.x: grid <= units, so in a chain it belongs to pass 0
-        const int u0 = blockIdx.x < total ? int(blockIdx.x) : total;
+        // single-pass launches: the first unit is blockIdx.x. Chained launches draw it too, so
+        // that every unit another CTA may wait for belongs to a CTA that is already running
+        // (drawing takes residency; launch order alone would not guarantee it).
+        int u0;
+        if constexpr (CHAIN) {
+            const int d0 = atomicAdd(p.work, 1) - p.work_base;
+            u0 = d0 < total ? d0 : total;
+        } else {
+            u0 = blockIdx.x < total ? int(blockIdx.x) : total;
+        }
         uq[0] = u0;
         if (u0 < total) {
-            const int d = int(gridDim.x) + atomicAdd(p.work, 1) - p.work_base;
+            const int d = (CHAIN ? 0 : int(gridDim.x)) + atomicAdd(p.work, 1) - p.work_base;
             drawn = d < total ? d : total;
         } else {
             drawn = total;
