@@ -969,11 +969,15 @@ struct TileGeom {
 };
 
 // Chained launches balance load across the whole pass sequence, not per pass, so their z
-// chunks need not be short: 8 chunks per column (>= 8 planes and >= the halo), measured best on
-// 128^3-256^3 (const7pt 256^3: 282 K MLUP/s at 8 chunks, 254 K at 16, 230 K at 4).
-int choose_zchunks_chained(int nzl, int H) {
-    const int len = std::max({8, H, (nzl + 7) / 8});
-    return std::max(1, (nzl + len - 1) / len);
+// chunks need not be short: at least 8 per column, more when the tile columns alone would
+// leave resident CTAs idle (about 1.5 units per CTA per pass), chunks at least max(H, 4)
+// planes. Measured (tools/small_sweep.sh, tools/chain_sweep.sh): const7pt 256^3 282 K MLUP/s
+// at 8 chunks (254 K at 16, 230 K at 4); const25pt 128^3 64 K at 16 (42 K at 8, 47 K at 32);
+// every kind at 64^3 best at 16 (4-plane chunks).
+int choose_zchunks_chained(int nzl, int H, int tiles_xy, int grid) {
+    int nzc = std::max(8, (3 * grid + 2 * tiles_xy - 1) / (2 * tiles_xy));
+    nzc = std::min(nzc, std::max(1, nzl / std::max(H, 4)));
+    return std::max(1, nzc);
 }
 
 TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max_grid,
@@ -988,7 +992,7 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
     t.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
-            : chained         ? choose_zchunks_chained(nzl, H)
+            : chained         ? choose_zchunks_chained(nzl, H, txy, max_grid)
                               : choose_zchunks(nzl, H, h.nc, txy, max_grid);
     t.zc_len = (nzl + t.nzc - 1) / t.nzc;
     t.nzc = (nzl + t.zc_len - 1) / t.zc_len;
