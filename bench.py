@@ -249,6 +249,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         tcfg.device = dev
         ds.set_config(tcfg)
         tuned = {"tb": tcfg.tb, "variant": tcfg.variant, "zchunks": tcfg.zchunks,
+                 "chain": tcfg.chain,
                  "mlups": tml, "measured": nmeas}
     for _ in range(args.warmup):
         ds.step(T)

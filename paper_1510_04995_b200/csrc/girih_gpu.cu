@@ -2345,18 +2345,24 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
             if (vt[i].tb <= tb_cap) vars.push_back(global_index_of(&vt[i]));
         const int zopts[] = {0, 1, 2, 4, 8, 16};
         const int nz_opts = int(sizeof(zopts) / sizeof(zopts[0]));
-        std::map<std::pair<int, int>, double> seen;
+        // scheduling axis, the counterpart of the reference tuning its wavefront variant
+        // (FED / relaxed, tuner.cpp:146-210): one launch per pass, or chained passes (the
+        // device TileScheduler); only single-slab handles can chain
+        const int copts[] = {-1, 1};
+        const int nc_opts = (h.slabs.size() == 1 && h.nranks == 1) ? 2 : 1;
+        std::map<std::array<int, 3>, double> seen;
         // adaptive_measure (tuner.cpp:47-71): double the test size until two runs agree
-        auto measure = [&](int vi, int zi) -> double {
-            auto key = std::make_pair(vi, zi);
+        auto measure = [&](int vi, int zi, int ci) -> double {
+            const std::array<int, 3> key{vi, zi, ci};
             if (auto it = seen.find(key); it != seen.end()) return it->second;
             const Variant* v = variant_by_global(vars[vi]);
             girih_gpu_config c = cfg_saved;
             c.tb = v->tb;
             c.variant = vars[vi];
             c.zchunks = zopts[zi];
+            c.chain = copts[ci];
             h.cfg = c;
-            long long steps = 2LL * v->tb;
+            long long steps = (c.chain > 0 ? 8LL : 2LL) * v->tb;
             girih_gpu_report r{};
             step_timed(h, steps, &r);  // warm-up
             double last = 0;
@@ -2375,26 +2381,31 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
             return last;
         };
         // hill_climb (tuner.cpp:73-104): axis-aligned, strict improvement, memoised
-        int bv = 0, bz = 0;
+        int bv = 0, bz = 0, bc = 0;
         for (size_t i = 0; i < vars.size(); ++i)  // start at the largest fused depth
             if (variant_by_global(vars[i])->tb >= variant_by_global(vars[bv])->tb) bv = int(i);
-        double bs = measure(bv, bz);
+        double bs = measure(bv, bz, bc);
         while (true) {
-            int nv2 = bv, nz2 = bz;
+            int nv2 = bv, nz2 = bz, nc2 = bc;
             double ns = bs;
-            const int cand[4][2] = {{bv - 1, bz}, {bv + 1, bz}, {bv, bz - 1}, {bv, bz + 1}};
+            const int cand[6][3] = {{bv - 1, bz, bc}, {bv + 1, bz, bc}, {bv, bz - 1, bc},
+                                    {bv, bz + 1, bc}, {bv, bz, bc - 1}, {bv, bz, bc + 1}};
             for (auto& c : cand) {
-                if (c[0] < 0 || c[0] >= int(vars.size()) || c[1] < 0 || c[1] >= nz_opts) continue;
-                const double sc = measure(c[0], c[1]);
+                if (c[0] < 0 || c[0] >= int(vars.size()) || c[1] < 0 || c[1] >= nz_opts ||
+                    c[2] < 0 || c[2] >= nc_opts)
+                    continue;
+                const double sc = measure(c[0], c[1], c[2]);
                 if (sc > ns) {
                     ns = sc;
                     nv2 = c[0];
                     nz2 = c[1];
+                    nc2 = c[2];
                 }
             }
-            if (nv2 == bv && nz2 == bz) break;
+            if (nv2 == bv && nz2 == bz && nc2 == bc) break;
             bv = nv2;
             bz = nz2;
+            bc = nc2;
             bs = ns;
         }
         // restore
@@ -2410,6 +2421,7 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         best->tb = variant_by_global(vars[bv])->tb;
         best->variant = vars[bv];
         best->zchunks = zopts[bz];
+        best->chain = copts[bc];
         if (best_mlups) *best_mlups = bs;
         if (n_measured) *n_measured = measured;
     });

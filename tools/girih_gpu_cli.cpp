@@ -220,7 +220,7 @@ std::string tuned_key(const Options& o) {
 }
 
 bool find_tuned(const std::string& path, const std::string& key, int* tb, int* variant,
-                int* zchunks) {
+                int* zchunks, int* chain = nullptr) {
     std::ifstream in(path);
     std::string line;
     while (std::getline(in, line)) {
@@ -233,6 +233,7 @@ bool find_tuned(const std::string& path, const std::string& key, int* tb, int* v
         *tb = field("tb");
         *variant = field("variant_index");
         *zchunks = field("zchunks");
+        if (chain) *chain = field("chain");  // absent in older records: 0 = auto
         return true;
     }
     return false;
@@ -245,7 +246,8 @@ int cmd_run(const Options& o) {
     cfg.tb = o.tb;
     cfg.variant = o.variant;
     if (!o.use_tuned.empty()) {
-        if (!find_tuned(o.use_tuned, tuned_key(o), &cfg.tb, &cfg.variant, &cfg.zchunks))
+        if (!find_tuned(o.use_tuned, tuned_key(o), &cfg.tb, &cfg.variant, &cfg.zchunks,
+                        &cfg.chain))
             throw std::runtime_error("no tuned configuration for this case in " + o.use_tuned +
                                      "; run `girih_gpu tune` first");
     }
@@ -327,10 +329,12 @@ int cmd_tune(const Options& o) {
     gpu::check(rc);
     std::ofstream os(out, std::ios::app);
     os << "{\"key\":" << key << ",\"best\":{\"tb\":" << best.tb << ",\"variant_index\":"
-       << best.variant << ",\"zchunks\":" << best.zchunks << ",\"mlups\":" << mlups
+       << best.variant << ",\"zchunks\":" << best.zchunks << ",\"chain\":" << best.chain
+       << ",\"mlups\":" << mlups
        << ",\"measured\":" << measured << "}}\n";
     std::cout << "tuned " << key << " tb=" << best.tb << " variant=" << best.variant
-              << " zchunks=" << best.zchunks << " mlups=" << mlups << '\n';
+              << " zchunks=" << best.zchunks << " chain=" << best.chain << " mlups=" << mlups
+              << '\n';
     return 0;
 }
 
