@@ -485,7 +485,8 @@ def test_chained_device_state_long_runs(girih, oracle):
         assert rp.n_launches == 300 and rc.n_launches == 3  # 128 + 128 + 44
 
 
-def test_ipc_halo_push_two_processes(girih):
+@pytest.mark.parametrize("nproc", [2, 3])
+def test_ipc_halo_push_two_processes(girih, nproc):
     # multi-process z-slabs without NCCL: each pass stores its boundary planes straight into
     # the neighbour rank's halo (CUDA IPC peer memory) and the ranks order their passes with
     # stream memory operations on each other's flags. Two ranks share this GPU here: their
@@ -494,8 +495,10 @@ def test_ipc_halo_push_two_processes(girih):
     import subprocess
     import sys
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29571", os.path.join(HERE, "ipc_worker.py")]
+    # (3 ranks: the middle one pushes to and waits for both neighbours)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={29571 + nproc}", os.path.join(HERE, "ipc_worker.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
-    assert out.stdout.count(": OK") == 2, out.stdout[-3000:]
+    assert out.stdout.count(": OK") == nproc, out.stdout[-3000:]
