@@ -2107,6 +2107,16 @@ int girih_gpu_ipc_connect(void* handle, const unsigned char* lower, const unsign
             n.zoff = b.zoff;
             n.open = true;
         }
+        // probe the stream memory operations on the mapped flags now (a no-op wait and a write
+        // of the initial value), so an unsupported setup fails here, before any rank steps,
+        // rather than in a pass its neighbours would wait for
+        {
+            const unsigned saved = h.epoch;
+            ipc_before_pass(h);  // waits for >= epoch: satisfied immediately
+            h.epoch = saved - 1;
+            ipc_after_pass(h);   // writes `saved` (the value the flags already hold)
+            h.epoch = saved;
+        }
         // the local state is fully initialised before any neighbour may push into it; the
         // caller barriers across ranks after every rank's connect
         GCHECK(cudaStreamSynchronize(s.stream));
