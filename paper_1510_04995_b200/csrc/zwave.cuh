@@ -46,6 +46,9 @@
 #ifndef GIRIH_CHAIN_MINB_DROP
 #define GIRIH_CHAIN_MINB_DROP 0  // A/B: chained kernels one resident CTA fewer (more registers)
 #endif
+#ifndef GIRIH_ZPS
+#define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
+#endif
 #ifndef GIRIH_XSHFL
 #define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
 #endif
@@ -572,13 +575,20 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     constexpr int CQD = CQ ? TB - 1 : 1, CQN = CQ ? 7 : 1;
     double2 cq[CQD][PPT][CQN], cnew[PPT][CQN];
     // per-thread z queues: zq[L][pair][d] = level L at plane (newest_L - 2R + d), d = 0..2R-1
-    double2 zq[TB][PPT][2 * R];
+    // ZPS (single-step radius-4 passes): the z+ neighbours k+1..k+R-1 are read from the level-0
+    // ring, which holds planes k..k+R anyway, so the queue keeps only k-R..k-1 (fewer registers;
+    // it is fed with the centre plane k instead of the newest plane). Measured (same box): the
+    // chained const25pt kernel stops spilling, +14-18% at 64^3-256^3; single-pass const25pt -1%,
+    // chained var25pt 128^3 -8%, so it is on for chained const25pt only.
+    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && KIND == K_CONST25 && CHAIN;
+    constexpr int ZQD = ZPS ? R : 2 * R;
+    double2 zq[TB][PPT][ZQD];
 #pragma unroll
     for (int L = 0; L < TB; ++L)
 #pragma unroll
         for (int i = 0; i < PPT; ++i)
 #pragma unroll
-            for (int d = 0; d < 2 * R; ++d) zq[L][i][d] = make_double2(0.0, 0.0);
+            for (int d = 0; d < ZQD; ++d) zq[L][i][d] = make_double2(0.0, 0.0);
 
     __syncthreads();  // uq[0] visible
     uint32_t g = G0;  // consumer's global element index
@@ -702,6 +712,12 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) newest[i] = pj[lcell[i] >> 1];
             }
+            double2 ctrk[ZPS ? PPT : 1];  // ZPS: level 0 at the centre plane k = j - R
+            if constexpr (ZPS) {
+                const double2* pk = reinterpret_cast<const double2*>(ring0 + ((g - R) % NR0) * CELLS);
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) ctrk[i] = pk[lcell[i] >> 1];
+            }
             // value of level L at its newest plane (j - L R) this iteration; the z queues advance
             // by one plane EVERY iteration so zq[L] always holds planes j-LR-2R .. j-LR-1 (entries
             // of planes a level did not compute are never read by a valid cell)
@@ -709,7 +725,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
             for (int L = 0; L < TB; ++L)
 #pragma unroll
-                for (int i = 0; i < PPT; ++i) fresh[L][i] = L == 0 ? newest[i] : make_double2(0.0, 0.0);
+                for (int i = 0; i < PPT; ++i)
+                    fresh[L][i] = L == 0 ? (ZPS ? ctrk[ZPS ? i : 0] : newest[i]) : make_double2(0.0, 0.0);
             bool staged = false;
             int ring_slot[TB];  // centre-ring slot each level writes this iteration (-1: none)
 #pragma unroll
@@ -786,6 +803,9 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     // holds k-R .. k+R-1 (oldest first), the newest (k+R) was produced above
                     auto Zp = [&](int dz) -> double2 {
                         if (dz == R) return newest[i];
+                        if (ZPS && dz > 0)
+                            return reinterpret_cast<const double2*>(
+                                ring0 + ((g - R + dz) % NR0) * CELLS)[lcell[i] >> 1];
                         return zq[s - 1][i][dz + R];
                     };
                     auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
@@ -919,7 +939,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         double* pen = (CHAIN ? SU2[seq & 1].dst_penult : p.dst_penult) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
-                            const double2 c2 = zq[TB - 1][i][R];  // level TB-1 at plane k
+                            // level TB-1 at plane k
+                            const double2 c2 = ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : R];
                             const int b = 2 * i;
                             if ((out_mask >> b) & 1 && !((ghost_mask >> b) & 1)) pen[colidx[b]] = c2.x;
                             if ((out_mask >> (b + 1)) & 1 && !((ghost_mask >> (b + 1)) & 1))
@@ -942,7 +963,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                                               : nullptr;
 #pragma unroll
                             for (int i = 0; i < PPT; ++i) {
-                                const double2 c2 = zq[TB - 1][i][R];
+                                const double2 c2 =
+                                    ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : R];
 #pragma unroll
                                 for (int q = 0; q < 2; ++q) {
                                     const int b = 2 * i + q;
@@ -983,8 +1005,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
 #pragma unroll
-                    for (int d = 0; d + 1 < 2 * R; ++d) zq[L][i][d] = zq[L][i][d + 1];
-                    zq[L][i][2 * R - 1] = fresh[L][i];
+                    for (int d = 0; d + 1 < ZQD; ++d) zq[L][i][d] = zq[L][i][d + 1];
+                    zq[L][i][ZQD - 1] = fresh[L][i];
                 }
             }
             if (tr) trp[2] = clock64();
