@@ -199,7 +199,11 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     kind = KINDS.index(args.stencil)
     n = args.n
     T = args.nt
-    dev = local_rank
+    # GIRIH_BENCH_SHARED_GPU=1: functional check of the multi-rank path with every rank on
+    # cuda:0 and gloo plumbing (tests only; such a run measures nothing and says so)
+    shared = os.environ.get("GIRIH_BENCH_SHARED_GPU") == "1"
+    dev = 0 if shared else local_rank
+    tdev = "cpu" if shared else "cuda"  # device of the small plumbing tensors
     hbm, hbm_src = measured_peaks()
     cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant)
     dist = None
@@ -213,7 +217,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(dev)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         ggrid = g.GridSpec(n, n, n * world)
         ds = None
         if args.halo == "push":
@@ -223,10 +230,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                 dist.all_gather_object(blobs, ds.ipc_export())
                 ds.ipc_connect(blobs[rank - 1] if rank > 0 else None,
                                blobs[rank + 1] if rank + 1 < world else None)
-                ok = torch.ones(1, device="cuda")
+                ok = torch.ones(1, device=tdev)
             except g.GirihError as e:
                 print(f"rank {rank}: IPC halo push unavailable ({e}); using NCCL", file=sys.stderr)
-                ok = torch.zeros(1, device="cuda")
+                ok = torch.zeros(1, device=tdev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() < 1 and ds is not None:  # every rank falls back together
                 ds.close()
@@ -234,7 +241,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
             dist.barrier()
             halo = "push" if ds is not None else None
         if ds is None:
-            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            idt = torch.zeros(128, dtype=torch.uint8, device=tdev)
             if rank == 0:
                 idt.copy_(torch.frombuffer(bytearray(g.nccl_unique_id()), dtype=torch.uint8))
             dist.broadcast(idt, 0)
@@ -266,7 +273,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
     kernel_s = sum(r.kernel_seconds for r in reps)
     if dist is not None:  # device time, max over ranks
-        tk = torch.tensor([kernel_s], dtype=torch.float64, device="cuda")
+        tk = torch.tensor([kernel_s], dtype=torch.float64, device=tdev)
         dist.all_reduce(tk, op=dist.ReduceOp.MAX)
         kernel_s = float(tk.item())
     cells = n ** 3  # per GPU
@@ -301,7 +308,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                 h2d, d2h = pr.h2d_bytes, pr.d2h_bytes
         wall = sum(walls) / len(walls)
         if dist is not None:
-            tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
+            tw = torch.tensor([wall], dtype=torch.float64, device=tdev)
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
             wall = float(tw.item())
         e2e = {"value": cells * world * T / wall / 1e6, "unit": "MLUP/s",
@@ -329,7 +336,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         "value": value, "unit": "MLUP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": kernel_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: device-generated init_state(seed 42) + SURVEY 8(d) remap",
+        "data": ("synthetic: device-generated init_state(seed 42) + SURVEY 8(d) remap" +
+                 ("; GIRIH_BENCH_SHARED_GPU functional check, all ranks on one GPU: NOT a "
+                  "measurement" if os.environ.get("GIRIH_BENCH_SHARED_GPU") == "1" else "")),
         "config": {"workload": f"BASELINE configs[1]: {KINDS[kind]} {n}^3 interior, T={T}, "
                                f"seed 42", "stencil": KINDS[kind], "n": n, "time_steps": T,
                    "tb": r0.tb_used, "variant": r0.variant_used, "zchunks": r0.zchunks_used,

@@ -502,3 +502,24 @@ def test_ipc_halo_push_two_processes(girih, nproc):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count(": OK") == nproc, out.stdout[-3000:]
+
+
+def test_bench_multirank_path_functional(girih):
+    # bench.py --gpus 2 under torchrun end to end (slab handles, IPC blob exchange, halo push,
+    # max-over-ranks timing, one JSON line), with both ranks sharing this GPU: a functional
+    # check of the driver's scaling path, labelled as no measurement in the line itself
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    env = dict(os.environ, GIRIH_BENCH_SHARED_GPU="1", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29631", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--no-e2e"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-3000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "NOT a measurement" in d["data"]
+    assert "pushed by each pass" in d["config"]["parallelism"]
