@@ -3,9 +3,13 @@
 // Replaces the reference's CPU execution engine girih::run (proj/src/engine.cpp:332-418):
 // instead of std::thread groups pulling diamond tiles from a dependency FIFO
 // (proj/src/scheduler.cpp:27-83), a host-side planner splits the run into passes of up to TB
-// fused time steps, and every pass is one persistent zwave kernel launch per z-slab whose CTAs
-// stream (x,y) tile columns along z (zwave.cuh). Multi-slab handles decompose z across
-// devices (or emulate it on one device) and exchange R*TB-deep halos between passes.
+// fused time steps, and every pass is a persistent zwave kernel whose CTAs stream (x,y) tile
+// columns along z (zwave.cuh). Runs of same-depth passes on small grids become one chained
+// launch whose units wait for their neighbourhood of the previous pass on the device (the
+// dependency FIFO's counterpart). Multi-slab handles decompose z across devices
+// or processes (or emulate it on one device); each pass pushes its R*TB-deep boundary planes
+// straight into the neighbours' halos (peer memory / CUDA IPC), with a copy / NCCL exchange
+// as the fallback. girih_gpu_run streams uploads, windowed passes and downloads along z.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
