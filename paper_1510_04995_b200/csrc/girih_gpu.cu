@@ -320,26 +320,25 @@ std::vector<Pass> make_plan(int kind, long long t0, long long steps, int tb) {
 // TMA descriptor encoding through the driver entry point (no -lcuda needed)
 // ------------------------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // thread-safe static initialisation; a throwing initialiser is retried on the next call
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         GCHECK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000,
                                                 cudaEnableDefault, &q));
         if (q != cudaDriverEntryPointSuccess || !p)
             throw_err(GIRIH_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
     return fn;
 }
 
 // L2 sector promotion of TMA fills (GIRIH_L2_PROMOTION = 0 / 64 / 128 / 256 overrides)
 CUtensorMapL2promotion l2_promotion() {
-    static int v = -1;
-    if (v < 0) {
+    static const int v = [] {
         const char* e = std::getenv("GIRIH_L2_PROMOTION");
-        v = e ? std::atoi(e) : 0;
-    }
+        return e ? std::atoi(e) : 0;
+    }();
     switch (v) {
     case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
@@ -563,9 +562,16 @@ struct NcclApi {
     decltype(&ncclGetErrorString) errorString = nullptr;
 };
 
+// lazily initialised process-wide tables (handles may live on several host threads)
+std::mutex& init_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
 NcclApi& nccl() {
     static NcclApi api;
     static bool loaded = false;
+    std::lock_guard<std::mutex> lk(init_mutex());
     if (loaded) return api;
     void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -956,6 +962,7 @@ struct LaunchInfo {
 // CTAs per SM of a variant (queried once per process and variant)
 int occupancy_of(const Variant* var, bool chained = false) {
     static std::map<std::pair<const Variant*, bool>, int> cache;
+    std::lock_guard<std::mutex> lk(init_mutex());
     auto it = cache.find({var, chained});
     if (it != cache.end()) return it->second;
     int occ = 0;

@@ -40,13 +40,10 @@ cudaError_t launch_zwave_impl(const CUtensorMap& cmap, const ChainDescs& cd, con
                               int grid, cudaStream_t stream) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
     auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(CFG::SMEM));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    // once per instantiation (thread-safe static initialisation)
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
+    if (attr != cudaSuccess) return attr;
     fn<<<grid, NT, CFG::SMEM, stream>>>(cmap, cd, p);
     return cudaGetLastError();
 }

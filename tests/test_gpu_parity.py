@@ -523,3 +523,35 @@ def test_bench_multirank_path_functional(girih):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and "NOT a measurement" in d["data"]
     assert "pushed by each pass" in d["config"]["parallelism"]
+
+
+def test_handles_on_concurrent_host_threads(girih, oracle):
+    # a handle belongs to one host thread (like girih::run's state), but independent handles
+    # may run on concurrent threads: lazily built process-wide tables (variant occupancy,
+    # driver entry points) are shared and guarded. Every thread's result is bitwise the oracle's.
+    import threading
+    g = girih
+    cases = [(k, tb) for k in range(4) for tb in tbs_for(g, k)][:8]
+    refs, errors = {}, []
+    for kind, tb in cases:
+        base = oracle.init_state(kind, 30, 26, 34, 1, 7 + kind, remap=True)
+        ref = base.copy()
+        oracle.naive_sweep(ref, 2 * tb + 1)
+        refs[(kind, tb)] = (base, ref)
+
+    def work(kind, tb):
+        try:
+            base, ref = refs[(kind, tb)]
+            for chain in (1, -1):
+                st = to_problem(g, base)
+                g.run(st, 2 * tb + 1, g.GpuConfig(tb=tb, chain=chain))
+                assert_state_equal(st, ref, f"thread {KIND_IDS[kind]} tb={tb} chain={chain}")
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=c) for c in cases]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
