@@ -526,6 +526,7 @@ struct Handle {
     } peer[2];
     std::unique_ptr<DevBuf> ipc_flags;  // ours: [0] = passes done by rank-1, [1] = by rank+1
     unsigned epoch = 0;                 // passes this rank has launched
+    bool ipc_connected = false;
     int sm_count = 0;
     // timing events (slab 0 stream)
     std::vector<cudaEvent_t> ev;
@@ -1229,6 +1230,8 @@ void order_slabs(Handle& h) {
 StepStats do_step(Handle& h, long long steps, bool time_passes) {
     StepStats st;
     if (steps == 0) return st;
+    if (h.ipc && !h.ipc_connected)
+        throw_err(GIRIH_ESTATE, "IPC slab handle used before girih_gpu_ipc_connect");
     const int tb = h.cfg.tb > 0 ? h.cfg.tb : default_tb_for(h);
     std::vector<Pass> plan = make_plan(h.kind, h.t_current, steps, tb);
     for (const Pass& ps : plan) {
@@ -2128,6 +2131,7 @@ int girih_gpu_ipc_connect(void* handle, const unsigned char* lower, const unsign
             ipc_after_pass(h);   // writes `saved` (the value the flags already hold)
             h.epoch = saved;
         }
+        h.ipc_connected = true;
         // the local state is fully initialised before any neighbour may push into it; the
         // caller barriers across ranks after every rank's connect
         GCHECK(cudaStreamSynchronize(s.stream));

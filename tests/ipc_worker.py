@@ -25,9 +25,14 @@ def main():
         with g.DeviceState.slab_seeded(kind, grid, 17, True, rank, world, None, cfg) as ds:
             blobs = [None] * world
             dist.all_gather_object(blobs, ds.ipc_export())
-            if not os.environ.get("GIRIH_IPC_NEGATIVE"):  # (negative control: no halo traffic)
-                ds.ipc_connect(blobs[rank - 1] if rank > 0 else None,
-                               blobs[rank + 1] if rank + 1 < world else None)
+            try:  # stepping an unconnected IPC slab is refused (its halos would go stale)
+                ds.step(1)
+                bad += 1
+                print(f"rank {rank}: step before ipc_connect was not refused", flush=True)
+            except g.GirihError:
+                pass
+            ds.ipc_connect(blobs[rank - 1] if rank > 0 else None,
+                           blobs[rank + 1] if rank + 1 < world else None)
             dist.barrier()
             ds.step(steps)
             ds.step(steps + 1)  # a second call: odd start level, pass counters carry over
