@@ -943,7 +943,9 @@ const CUtensorMap& tensor_map(Handle& h, int slab, const double* base, int narr,
 int choose_zchunks(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
     // coefficient-heavy kinds: each chunk boundary re-streams (TB-1)R coefficient planes that
     // no longer sit in L2 (16.8 MB per 512^2 plane for var7pt), so their chunks are longer
-    int len = ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
+    // radius 4: every chunk re-streams 2H = 8+ extra planes, so chunks are longer still
+    // (const25pt 512^3: 139.8 K MLUP/s at ~48-plane chunks vs 134.8 K at 32; var25pt +1%)
+    int len = H >= 4 ? 12 * H : ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
     // small grids: shorten chunks (in ~20% steps) until there are enough units per resident
     // CTA that the last unit's tail is short against the pass: 5 for the light kinds
     // (const7pt 256^3 +3%, const25pt 256^3 +10% over 2), 2 for the coefficient-heavy ones,
