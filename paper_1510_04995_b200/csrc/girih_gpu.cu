@@ -945,7 +945,11 @@ int choose_zchunks(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
     // no longer sit in L2 (16.8 MB per 512^2 plane for var7pt), so their chunks are longer
     // radius 4: every chunk re-streams 2H = 8+ extra planes, so chunks are longer still
     // (const25pt 512^3: 139.8 K MLUP/s at ~48-plane chunks vs 134.8 K at 32; var25pt +1%)
-    int len = H >= 4 ? 12 * H : ncoeff >= 7 ? std::max(32, 8 * H) : std::max(16, 8 * H);
+    // (measured optima: const7pt 512^3 ~22-plane chunks +2.8% over 16; var7pt 768^3-1024^3 ~40
+    // +1.5-3% over 32, but 32 below: 256^3 -5% and 384^3 -1.5% at 40)
+    int len = H >= 4 ? 12 * H
+              : ncoeff >= 7 ? std::max(nzl > 512 ? 40 : 32, 8 * H)
+                            : std::max(24, 8 * H);
     // small grids: shorten chunks (in ~20% steps) until there are enough units per resident
     // CTA that the last unit's tail is short against the pass: 5 for the light kinds
     // (const7pt 256^3 +3%, const25pt 256^3 +10% over 2), 2 for the coefficient-heavy ones,
@@ -988,8 +992,10 @@ struct TileGeom {
 // planes. Measured (tools/small_sweep.sh, tools/chain_sweep.sh): const7pt 256^3 282 K MLUP/s
 // at 8 chunks (254 K at 16, 230 K at 4); const25pt 128^3 64 K at 16 (42 K at 8, 47 K at 32);
 // every kind at 64^3 best at 16 (4-plane chunks).
-int choose_zchunks_chained(int nzl, int H, int tiles_xy, int grid) {
-    int nzc = std::max(8, (3 * grid + 2 * tiles_xy - 1) / (2 * tiles_xy));
+int choose_zchunks_chained(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
+    // const25pt re-streams 2H = 8 halo planes per chunk: 6 (256^3: 128 K vs 124 K at 8; var25pt
+    // keeps 8: 128^3 -7% at 7)
+    int nzc = std::max(H >= 4 && ncoeff < 7 ? 6 : 8, (3 * grid + 2 * tiles_xy - 1) / (2 * tiles_xy));
     nzc = std::min(nzc, std::max(1, nzl / std::max(H, 4)));
     return std::max(1, nzc);
 }
@@ -1006,7 +1012,7 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
     t.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
-            : chained         ? choose_zchunks_chained(nzl, H, txy, max_grid)
+            : chained         ? choose_zchunks_chained(nzl, H, h.nc, txy, max_grid)
                               : choose_zchunks(nzl, H, h.nc, txy, max_grid);
     t.zc_len = (nzl + t.nzc - 1) / t.nzc;
     t.nzc = (nzl + t.zc_len - 1) / t.zc_len;
