@@ -69,6 +69,9 @@ for kind in [int(k) for k in a.kinds.split(",")]:
                 nd = ds.compare("u", ref.u)[0] + ds.compare("v", ref.v)[0]
             rec["parity"] = nd == 0
             rec["parity_kind"] = "bitwise single-domain vs 8 emulated z-slabs (u and v)"
+            del ref  # 17 GB of pinned host memory at var25pt 1024^3
+            import gc
+            gc.collect()
         elif a.parity and n == 256:
             outs = []
             for slabs in (0, 2):
