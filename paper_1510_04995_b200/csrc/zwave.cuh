@@ -42,9 +42,13 @@
 
 #include <cuda.h>
 #include <cstdint>
+#include <type_traits>
 
 #ifndef GIRIH_CHAIN_MINB_DROP
 #define GIRIH_CHAIN_MINB_DROP 0  // A/B: chained kernels one resident CTA fewer (more registers)
+#endif
+#ifndef GIRIH_PHZ
+#define GIRIH_PHZ 1  // single-pass const25pt: z queue rotated by renaming (see PHZ)
 #endif
 #ifndef GIRIH_ZPS
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
@@ -324,6 +328,14 @@ __device__ __forceinline__ void chain_acquire() {
 
 template <int KIND> struct STACK_OK { static constexpr bool value = true; };
 
+// calls f(integral_constant<I>), f(integral_constant<I+1>), ... while f returns true
+template <int I, int N, class F>
+__device__ __forceinline__ void unroll_phases(F& f) {
+    if constexpr (I < N) {
+        if (f(std::integral_constant<int, I>{})) unroll_phases<I + 1, N>(f);
+    }
+}
+
 template <int KIND> struct AuxArrays { static constexpr int N = KindTraits<KIND>::NC; };
 template <> struct AuxArrays<K_CONST25> { static constexpr int N = 2; };  // C and level t0-1
 
@@ -580,7 +592,11 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     // it is fed with the centre plane k instead of the newest plane). Measured (same box): the
     // chained const25pt kernel stops spilling, +14-18% at 64^3-256^3; single-pass const25pt -1%,
     // chained var25pt 128^3 -8%, so it is on for chained const25pt only.
-    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && KIND == K_CONST25 && CHAIN;
+    // PHZ (single-pass const25pt): the 4-entry z- queue rotates by renaming over 4 unrolled
+    // iteration phases instead of 64 register moves per warp-iteration; it needs ZPS's short
+    // queue to fit the register budget (the 8-entry version spilled)
+    constexpr bool PHZ = GIRIH_PHZ && TB == 1 && KIND == K_CONST25 && !CHAIN;
+    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && KIND == K_CONST25 && (CHAIN || PHZ);
     constexpr int ZQD = ZPS ? R : 2 * R;
     double2 zq[TB][PPT][ZQD];
 #pragma unroll
@@ -637,7 +653,9 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         const bool any_ghost_col = __syncthreads_or(col_fix != 0);
         const bool any_odd_col = (p.nx & 1) && ug.tx == p.tiles_x - 1;  // owner of the last column
 
-        for (int it = 0; it < n_it; ++it, ++g) {
+        // one z-plane iteration; PH = phase of the rotating z queue (always 0 unless PHZ)
+        auto iteration = [&](auto PHc, const int it) {
+            constexpr int PH = decltype(PHc)::value;
             const int j = ug.za - H + it;  // level-0 plane of this iteration
             __syncthreads();               // previous iteration's smem reads/writes are complete
 #ifdef GIRIH_ZWAVE_TRACE
@@ -806,7 +824,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         if (ZPS && dz > 0)
                             return reinterpret_cast<const double2*>(
                                 ring0 + ((g - R + dz) % NR0) * CELLS)[lcell[i] >> 1];
-                        return zq[s - 1][i][dz + R];
+                        return zq[s - 1][i][(dz + R + PH) % ZQD];
                     };
                     auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
                     auto comp = [](const double2& v, int q) -> double { return q ? v.y : v.x; };
@@ -857,7 +875,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         const double2 cf = Cp(0);
                         // level s-2 at plane k: t0-1 from the aux ring (s = 1), else the oldest
                         // entry of level s-2's z queue (before this iteration's shift)
-                        const double2 up = s == 1 ? Cp(1) : zq[s >= 2 ? s - 2 : 0][i][0];
+                        const double2 up = s == 1 ? Cp(1) : zq[s >= 2 ? s - 2 : 0][i][PH % ZQD];
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
                             const double vc = X(q, 0);
@@ -940,7 +958,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
                             // level TB-1 at plane k
-                            const double2 c2 = ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : R];
+                            const double2 c2 = ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : (R + PH) % ZQD];
                             const int b = 2 * i;
                             if ((out_mask >> b) & 1 && !((ghost_mask >> b) & 1)) pen[colidx[b]] = c2.x;
                             if ((out_mask >> (b + 1)) & 1 && !((ghost_mask >> (b + 1)) & 1))
@@ -964,7 +982,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
                             for (int i = 0; i < PPT; ++i) {
                                 const double2 c2 =
-                                    ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : R];
+                                    ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : (R + PH) % ZQD];
 #pragma unroll
                                 for (int q = 0; q < 2; ++q) {
                                     const int b = 2 * i + q;
@@ -1004,9 +1022,13 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             for (int L = 0; L < TB; ++L) {
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) {
+                    if constexpr (PHZ) {
+                        zq[L][i][PH % ZQD] = fresh[L][i];  // the oldest entry's slot
+                    } else {
 #pragma unroll
-                    for (int d = 0; d + 1 < ZQD; ++d) zq[L][i][d] = zq[L][i][d + 1];
-                    zq[L][i][ZQD - 1] = fresh[L][i];
+                        for (int d = 0; d + 1 < ZQD; ++d) zq[L][i][d] = zq[L][i][d + 1];
+                        zq[L][i][ZQD - 1] = fresh[L][i];
+                    }
                 }
             }
             if (tr) trp[2] = clock64();
@@ -1034,6 +1056,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     bulk_wait_read_all();
             }
             if (tr) trp[3] = clock64();
+            ++g;
+        };
+        constexpr int NPH = PHZ ? ZQD : 1;
+        for (int it0 = 0; it0 < n_it; it0 += NPH) {
+            auto phase = [&](auto PHc) -> bool {
+                if (it0 + decltype(PHc)::value >= n_it) return false;
+                iteration(PHc, it0 + decltype(PHc)::value);
+                return true;
+            };
+            unroll_phases<0, NPH>(phase);
         }
     }
     __syncthreads();
