@@ -50,6 +50,9 @@
 #ifndef GIRIH_PHZ
 #define GIRIH_PHZ 1  // single-pass const25pt: z queue rotated by renaming (see PHZ)
 #endif
+#ifndef GIRIH_PHZ_ALL
+#define GIRIH_PHZ_ALL 0  // A/B: PHZ for every single-step radius-4 kernel
+#endif
 #ifndef GIRIH_ZPS
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
 #endif
@@ -595,8 +598,9 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     // PHZ (single-pass const25pt): the 4-entry z- queue rotates by renaming over 4 unrolled
     // iteration phases instead of 64 register moves per warp-iteration; it needs ZPS's short
     // queue to fit the register budget (the 8-entry version spilled)
-    constexpr bool PHZ = GIRIH_PHZ && TB == 1 && KIND == K_CONST25 && !CHAIN;
-    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && KIND == K_CONST25 && (CHAIN || PHZ);
+    constexpr bool PHZ = GIRIH_PHZ && TB == 1 &&
+                         (GIRIH_PHZ_ALL ? R == 4 : (KIND == K_CONST25 && !CHAIN));
+    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && ((KIND == K_CONST25 && CHAIN) || PHZ);
     constexpr int ZQD = ZPS ? R : 2 * R;
     double2 zq[TB][PPT][ZQD];
 #pragma unroll
