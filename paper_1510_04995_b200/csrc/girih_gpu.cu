@@ -947,8 +947,10 @@ int choose_zchunks(int nzl, int H, int ncoeff, int tiles_xy, int grid) {
     // (const25pt 512^3: 139.8 K MLUP/s at ~48-plane chunks vs 134.8 K at 32; var25pt +1%)
     // (measured optima: const7pt 512^3 ~22-plane chunks +2.8% over 16; var7pt 768^3-1024^3 ~40
     // +1.5-3% over 32, but 32 below: 256^3 -5% and 384^3 -1.5% at 40)
+    // (var7pt with the 64x18 tile: 64-plane chunks from 384^3 on, bench +6% over 32 at 512^3,
+    // 384^3 +3%; ~40 below)
     int len = H >= 4 ? 12 * H
-              : ncoeff >= 7 ? std::max(nzl > 512 ? 40 : 32, 8 * H)
+              : ncoeff >= 7 ? std::max(nzl >= 384 ? 64 : 40, 8 * H)
                             : std::max(24, 8 * H);
     // small grids: shorten chunks (in ~20% steps) until there are enough units per resident
     // CTA that the last unit's tail is short against the pass: 5 for the light kinds

@@ -9,9 +9,9 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT(K_VAR7, 1, 64, 8, 96, 3, 1, 3),
     GIRIH_VARIANT(K_VAR7, 1, 64, 10, 128, 3, 1, 2),
     GIRIH_VARIANT(K_VAR7, 1, 64, 16, 224, 4, 1, 1),
+    GIRIH_VARIANT(K_VAR7, 2, 64, 18, 512, 2, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 2, 2, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 448, 3, 2, 1),
-    GIRIH_VARIANT(K_VAR7, 2, 64, 18, 512, 2, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 18, 512, 3, 1, 1),
     GIRIH_VARIANT(K_VAR7, 2, 64, 16, 224, 2, 2, 1),
     GIRIH_VARIANT(K_VAR7, 2, 32, 32, 480, 2, 2, 1),
