@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GIRIH_GPU_ABI_VERSION 2
+#define GIRIH_GPU_ABI_VERSION 3
 
 #define GIRIH_OK 0
 #define GIRIH_EINVAL (-1)
@@ -98,6 +98,10 @@ typedef struct {
 typedef struct {
     int kind, tb, lx, ly, threads, prefetch;
     int smem_bytes;
+    int cluster_y;          /* CTAs per thread-block cluster along y (1 = none): the cluster's
+                               CTAs share the fused levels' halo rows through distributed
+                               shared memory */
+    int aux_prefetch;       /* coefficient planes fetched ahead */
 } girih_gpu_variant;
 
 const char* girih_gpu_last_error(void);
@@ -159,6 +163,12 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
                       long long* first_index);
 
 /* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
+/* Device-side digest of a whole field (0 = u, 1 = v, 2 + c = coefficient c), ghosts and pad
+ * included: FNV-1a over the FNV-1a hashes of every allocated row in (k, j) order (one GPU
+ * thread per row). A checksum of checksums of the full state that needs no download; the
+ * oracle computes the same function on host arrays (orc_row_digest). */
+int girih_gpu_row_digest(void* handle, int field, unsigned long long* digest);
+
 int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double* cc);
 
 int girih_gpu_get_t(void* handle, long long* t_current);

@@ -227,3 +227,18 @@ uint64_t orc_fnv_all(const double* f, uint64_t n) {
     }
     return h;
 }
+
+/* Row digest: FNV-1a of every row's bytes (rows of row_elems doubles, in k, j order), then
+ * FNV-1a over the little-endian bytes of those row hashes. Test helper: a checksum of
+ * checksums that a GPU can also compute in parallel, one thread per row (girih_gpu_row_digest). */
+uint64_t orc_row_digest(const double* f, uint64_t nrows, uint64_t row_elems) {
+    uint64_t d = 0xCBF29CE484222325ull;
+    for (uint64_t r = 0; r < nrows; ++r) {
+        const uint64_t h = orc_fnv_all(f + r * row_elems, row_elems);
+        for (int b = 0; b < 8; ++b) {
+            d ^= (h >> (8 * b)) & 0xFF;
+            d *= 0x100000001B3ull;
+        }
+    }
+    return d;
+}

@@ -16,6 +16,10 @@ cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, i
                                  unsigned long long* count, unsigned long long* first,
                                  int sm_count, cudaStream_t stream);
 
+// per-row FNV-1a hashes of local planes [k0, k0+nk) (rows in k, j order) into out[nk * Y]
+cudaError_t launch_row_fnv(const double* dev, int pitch, int off, int X, int Y, int k0, int nk,
+                           unsigned long long* out, cudaStream_t stream);
+
 // ghost shell (ghost planes, ghost rows, ghost/pad columns) of allocated planes [k0, k0+nk) from
 // a packed host-order block (see init_kernels.cu)
 cudaError_t launch_scatter_shell(double* dev, int pitch, int off, int X, int Y, int R, int nx,

@@ -18,9 +18,14 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -156,13 +161,19 @@ const Variant* select_variant(int kind, int tb, int requested) {
 // CTA's 128-register cap, so chains take the 224-thread 64x16 tile (254 registers, no spill):
 // 128^3 72 K vs 59 K MLUP/s one launch per pass, 64^3 24 K vs 18 K.
 const Variant* select_chain_variant(int kind, int tb, int requested) {
+    int n;
+    const Variant* t = variant_table(kind, &n);
     if (requested < 0 && kind == K_VAR7 && tb == 2) {
-        int n;
-        const Variant* t = variant_table(kind, &n);
         for (int i = 0; i < n; ++i)
             if (t[i].tb == 2 && t[i].lx == 64 && t[i].ly == 16 && t[i].threads == 224) return &t[i];
     }
-    return select_variant(kind, tb, requested);
+    const Variant* v = select_variant(kind, tb, requested);
+    if (v->cy > 1) {  // cluster kernels run single passes: the best non-cluster tile instead
+        for (int i = 0; i < n; ++i)
+            if (t[i].tb == v->tb && t[i].cy == 1) return &t[i];
+        return nullptr;
+    }
+    return v;
 }
 
 inline int parity_of(long long t) { return int(((t % 2) + 2) % 2); }
@@ -760,6 +771,77 @@ void ensure_scratch(Handle& h, int parity) {
 // Flat device staging buffer for host copies: a host->device copy into the pitched layout runs
 // at ~32 GB/s as a 2-D copy but at full PCIe rate (~55 GB/s) flat, followed by an on-device 2-D
 // copy. Falls back to the direct 2-D copy when the buffer cannot be allocated.
+// ---- host link for the drop-in call. Page-locked (pinned) caller buffers are read and written
+// by the copy engines directly. Pageable ones -- what the reference's ProblemState holds
+// (std::vector, stencil.hpp:47-98) -- go through page-locked bounce blocks that host threads
+// fill and drain with a parallel memcpy: the driver's own pageable path stages serially and
+// blocks the issuing thread. ----
+bool host_is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int host_copy_threads() {
+    static const int n = [] {
+        if (const char* e = std::getenv("GIRIH_HOST_THREADS")) return std::max(1, std::atoi(e));
+        return std::max(1, std::min(16, int(std::thread::hardware_concurrency())));
+    }();
+    return n;
+}
+
+// memcpy split over the host copy threads (pieces >= 4 MB)
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const int nt = int(std::min<size_t>(host_copy_threads(), std::max<size_t>(1, bytes >> 22)));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t piece = (bytes + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) {
+        const size_t a = size_t(t) * piece, n = std::min(piece, bytes - std::min(bytes, a));
+        if (n) th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a,
+                                                 static_cast<const char*>(src) + a, n); });
+    }
+    std::memcpy(dst, src, std::min(piece, bytes));
+    for (auto& t : th) t.join();
+}
+
+// page-locked bounce blocks (grow-only, process-wide; used under pinned_scratch_mutex())
+struct BouncePool {
+    std::vector<void*> blocks;
+    size_t bytes = 0;
+};
+BouncePool& bounce_pool(int which) {
+    static BouncePool pools[2];  // 0: uploads, 1: downloads
+    return pools[which];
+}
+// n blocks of at least `bytes`; nullptr when page-locked memory cannot be had
+void* const* bounce_blocks(int which, int n, size_t bytes) {
+    BouncePool& bp = bounce_pool(which);
+    if (int(bp.blocks.size()) < n || bp.bytes < bytes) {
+        for (void* q : bp.blocks) cudaFreeHost(q);
+        bp.blocks.clear();
+        bp.bytes = 0;
+        for (int i = 0; i < n; ++i) {
+            void* q = nullptr;
+            if (cudaMallocHost(&q, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                for (void* r : bp.blocks) cudaFreeHost(r);
+                bp.blocks.clear();
+                return nullptr;
+            }
+            bp.blocks.push_back(q);
+        }
+        bp.bytes = bytes;
+    }
+    return bp.blocks.data();
+}
+
 double* host_stage(Handle& h, Slab& s) {
     if (s.hstage) return s.hstage->p;
     if (s.hstage_failed) return nullptr;
@@ -968,16 +1050,20 @@ struct LaunchInfo {
     long long computed_lups = 0;
 };
 
-// CTAs per SM of a variant (queried once per process and variant)
-int occupancy_of(const Variant* var, bool chained = false) {
-    static std::map<std::pair<const Variant*, bool>, int> cache;
+// Resident CTAs of a variant on the device (the persistent grid limit; for cluster variants
+// whole clusters, from cudaOccupancyMaxActiveClusters). Queried once per process, device and
+// variant.
+int max_resident_ctas(const Variant* var, bool chained = false) {
+    static std::map<std::tuple<const Variant*, bool, int>, int> cache;
     std::lock_guard<std::mutex> lk(init_mutex());
-    auto it = cache.find({var, chained});
+    int dev = 0;
+    GCHECK(cudaGetDevice(&dev));
+    auto it = cache.find({var, chained, dev});
     if (it != cache.end()) return it->second;
     int occ = 0;
     GCHECK((chained ? var->occupancy_chain : var->occupancy)(&occ));
-    if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on an SM");
-    cache[{var, chained}] = occ;
+    if (occ < 1) throw_err(GIRIH_ECUDA, "zwave variant does not fit on the device");
+    cache[{var, chained, dev}] = occ;
     return occ;
 }
 
@@ -1009,10 +1095,14 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
     t.hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
     t.ox = var->lx - 2 * t.hx;
-    t.oy = var->ly - 2 * H;
+    // y: one tile = one CTA, or one cluster of cy CTAs whose boxes overlap by 2R rows and
+    // share the fused levels' halo rows (zwave.cuh ZwaveConfig::OYC)
+    t.oy = var->cy > 1 ? var->cy * (var->ly - 2 * R) - 2 * (tb - 1) * R : var->ly - 2 * H;
     t.tiles_x = (h.nx + t.ox - 1) / t.ox;
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
+    // units are per cluster: the z-chunk heuristics count clusters as the resident "CTAs"
+    max_grid = std::max(1, max_grid / var->cy);
     t.nzc = h.cfg.zchunks > 0 ? std::min(h.cfg.zchunks, nzl)
             : chained         ? choose_zchunks_chained(nzl, H, h.nc, txy, max_grid)
                               : choose_zchunks(nzl, H, h.nc, txy, max_grid);
@@ -1041,7 +1131,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         zhi = s.zout_hi;
     }
     const int nzl = zhi - zlo;
-    const int max_grid = h.sm_count * occupancy_of(var, chained);
+    const int max_grid = max_resident_ctas(var, chained);
     const TileGeom tg = tile_geom(h, ps.tb, var, nzl, max_grid, chained);
     const int hx = tg.hx, OX = tg.ox;
     PassParams p{};
@@ -1109,10 +1199,33 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         }
         p.push_hz = h.hz;
     }
-    li->grid = std::min(p.units, max_grid);
+    // cluster variants: cy CTAs per unit, the grid a whole number of clusters
+    li->grid = std::min(p.units * var->cy, max_grid / var->cy * var->cy);
     li->zchunks = p.nzc;
     li->computed_lups = tg.computed_lups;
     return p;
+}
+
+// The per-pass descriptor of a single-pass launch. Output maps: the store box is the output
+// tile of one CTA; cluster variants have two heights (outer CTAs keep the trapezoid halo on
+// their outer side, inner CTAs store all their own rows).
+PassDesc single_desc(Handle& h, int slab, const Variant* var, int tb, const PassParams& p,
+                     const CUtensorMap& vmap, const CUtensorMap& umap) {
+    PassDesc d{};
+    d.vmap = vmap;
+    d.umap = umap;
+    const int R = h.R, H = tb * R;
+    if (var->cy > 1) {
+        d.omap = tensor_map(h, slab, p.dst_final, 1, p.ox, var->ly - R - H, 1);
+        d.omap_in = tensor_map(h, slab, p.dst_final, 1, p.ox, var->ly - 2 * R, 1);
+    } else {
+        d.omap = tensor_map(h, slab, p.dst_final, 1, p.ox, var->ly - 2 * H, 1);
+        d.omap_in = d.omap;
+    }
+    d.dst_final = p.dst_final;
+    d.dst_penult = p.dst_penult;
+    d.parity0 = p.parity0;
+    return d;
 }
 
 }  // namespace
@@ -1344,10 +1457,12 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
         st.variant = global_index_of(var);
         st.tb_used = std::max(st.tb_used, ps.tb);
-        if (can_chain) {
-            const Variant* cvar = select_chain_variant(
-                h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
-            if (cvar->tb != ps.tb) cvar = select_chain_variant(h.kind, ps.tb, -1);
+        const Variant* cvar =
+            can_chain ? select_chain_variant(h.kind, ps.tb,
+                                             (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1)
+                      : nullptr;
+        if (cvar && cvar->tb != ps.tb) cvar = select_chain_variant(h.kind, ps.tb, -1);
+        if (cvar) {
             // the longest run of passes with this depth (same variant and tile grid) that fits
             // one launch: <= CHAIN_MAX passes, <= CHAIN_DESC distinct buffer sets
             std::vector<std::array<int, 5>> keys;
@@ -1388,6 +1503,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                                                            cvar->aux_x, cvar->aux_y)
                                               : d.vmap;
                     d.omap = tensor_map(h, 0, s.buf[pf.dst]->p, 1, p.ox, cvar->ly - 2 * pf.tb * h.R, 1);
+                    d.omap_in = d.omap;
                     d.dst_final = s.buf[pf.dst]->p;
                     d.dst_penult = pf.dst_penult >= 0 ? s.buf[pf.dst_penult]->p : nullptr;
                     d.parity0 = parity_of(tk);
@@ -1396,6 +1512,10 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 cd.npass = npass;
                 cd.done = reinterpret_cast<int*>(s.chain_done->p);
                 GCHECK(cudaMemsetAsync(cd.done, 0, size_t(npass) * p.nzc * sizeof(int), s.stream));
+                if (work_base[0] + (long long)npass * p.units + li.grid > (1ll << 30)) {
+                    GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+                    work_base[0] = 0;
+                }
                 p.work_base = int(work_base[0]);
                 // every unit is drawn, plus one failing draw per CTA
                 work_base[0] += (long long)npass * p.units + li.grid;
@@ -1425,6 +1545,10 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             GCHECK(cudaSetDevice(s.device));
             LaunchInfo li;
             PassParams p = build_params(h, ps, var, int(g), t, &li);
+            if (work_base[g] + p.units > (1ll << 30)) {  // long runs: restart the unit counter
+                GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+                work_base[g] = 0;
+            }
             p.work_base = int(work_base[g]);
             work_base[g] += p.units;
             const CUtensorMap& vmap = tensor_map(h, int(g), s.buf[ps.src]->p, 1, var->lx, var->ly);
@@ -1435,14 +1559,13 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                                    var->aux_x, var->aux_y);
             if (ps.src_prev >= 0)
                 umap = &tensor_map(h, int(g), s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
-            const CUtensorMap& omap = tensor_map(h, int(g), s.buf[ps.dst]->p, 1, p.ox,
-                                                 var->ly - 2 * ps.tb * h.R, 1);
             // inside a stream capture a plain record only orders streams: record as graph nodes
             const unsigned evflag = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
             if (h.ipc) ipc_before_pass(h);
             if (time_passes && g == 0)
                 GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
-            GCHECK(var->launch(vmap, *cmap, *umap, omap, p, li.grid, s.stream));
+            const PassDesc pd = single_desc(h, int(g), var, ps.tb, p, vmap, *umap);
+            GCHECK(var->launch(*cmap, pd, p, li.grid, s.stream));
             if (time_passes && g == 0)
                 GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
             if (p.trace) {  // debug: dump CTA 0's phase clocks of this pass
@@ -1587,8 +1710,10 @@ bool stream_run_eligible(const Handle& h, long long steps) {
     const bool tb_ok = h.kind == K_CONST25 ? (h.cfg.tb == 0 || h.cfg.tb == 1)
                                            : (h.cfg.tb == 0 || h.cfg.tb == 1 ||
                                               (h.cfg.tb == 2 && h.R == 1));
+    // the windows slide by the stencil reach of every pass, so their count (and the task
+    // graph's streams and events) grows with steps * R: long runs take the plain path
     return h.slabs.size() == 1 && h.nranks == 1 && !h.emulated && tb_ok && steps >= 4 &&
-           h.nz >= 64 && !std::getenv("GIRIH_NO_STREAM_RUN");
+           steps * h.R <= 2LL * h.nz && h.nz >= 64 && !std::getenv("GIRIH_NO_STREAM_RUN");
 }
 
 void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu_report* rep) {
@@ -1702,12 +1827,42 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         }
     } ev_guard{ev_h2d, ev_free};
     GCHECK(cudaEventRecord(t_up0, up));
-    int nup = 0;
+    // caller memory: page-locked buffers are copied by the DMA engines directly; pageable ones
+    // (a reference ProblemState's std::vectors) through page-locked bounce blocks
+    bool pinned_in = host_is_pinned(v.u) && host_is_pinned(v.v);
+    for (int c = 0; c < h.nc; ++c) pinned_in = pinned_in && host_is_pinned(v.coeffs[c]);
+    const bool pinned_out = host_is_pinned(v.u) && host_is_pinned(v.v);
+    const size_t chunk_bytes = size_t(W) * hplane * 8;
+    constexpr int NBU = 3, NBD = 4;  // upload / download bounce blocks of one chunk each
+    // (no page-locked memory to be had: the driver's own pageable path)
+    void* const* ubounce = pinned_in ? nullptr : bounce_blocks(0, NBU, chunk_bytes);
+    void* const* dbounce = pinned_out ? nullptr : bounce_blocks(1, NBD, chunk_bytes);
+    cudaEvent_t ev_ub[NBU], ev_db[NBD];
+    for (auto& e : ev_ub) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev_db) GCHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct BounceEventGuard {
+        cudaEvent_t* a;
+        cudaEvent_t* b;
+        ~BounceEventGuard() {
+            for (int i = 0; i < NBU; ++i) cudaEventDestroy(a[i]);
+            for (int i = 0; i < NBD; ++i) cudaEventDestroy(b[i]);
+        }
+    } bounce_guard{ev_ub, ev_db};
+    int nup = 0, nub = 0;
     auto upload_chunk = [&](double* dev, const double* host, int k0, int nk) {
         const int i = nup++ & 1;
         if (nup > 2) GCHECK(cudaStreamWaitEvent(up, ev_free[i], 0));  // staging block reusable
-        GCHECK(cudaMemcpyAsync(stage[i]->p, host + size_t(k0) * hplane, size_t(nk) * hplane * 8,
-                               cudaMemcpyHostToDevice, up));
+        const size_t bytes = size_t(nk) * hplane * 8;
+        const double* src = host + size_t(k0) * hplane;
+        if (ubounce) {
+            const int j = nub++ % NBU;
+            if (nub > NBU) GCHECK(cudaEventSynchronize(ev_ub[j]));  // its last H2D has read it
+            parallel_memcpy(ubounce[j], src, bytes);
+            GCHECK(cudaMemcpyAsync(stage[i]->p, ubounce[j], bytes, cudaMemcpyHostToDevice, up));
+            GCHECK(cudaEventRecord(ev_ub[j], up));
+        } else {
+            GCHECK(cudaMemcpyAsync(stage[i]->p, src, bytes, cudaMemcpyHostToDevice, up));
+        }
         GCHECK(cudaEventRecord(ev_h2d[i], up));
         GCHECK(cudaStreamWaitEvent(scat, ev_h2d[i], 0));
         GCHECK(cudaMemcpy2DAsync(dev + (size_t)k0 * pe + h.off, size_t(h.pitch) * 8, stage[i]->p,
@@ -1767,21 +1922,48 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                                     nk, dshell->p, scat));
         GCHECK(cudaEventRecord(ev_free[i], scat));
     };
-    for (int d = 0; d < nchunk; ++d) {
-        const int k0 = d * W, nk = std::min(W, h.Z - k0);
-        for (int c = 0; c < h.nc; ++c) upload_chunk(s.coeff(c, h.slab_elems(s)), v.coeffs[c], k0, nk);
-        upload_chunk(s.buf[b]->p, b == 0 ? v.u : v.v, k0, nk);
-        if (shell)
-            upload_shell(k0, nk);
-        else
-            upload_chunk(other, host_other, k0, nk);
-        for (int r = 1; r < 3 && !single; ++r)
-            GCHECK(cudaMemcpyAsync(rot[r] + (size_t)k0 * pe, rot[0] + (size_t)k0 * pe,
-                                   size_t(nk) * pe * 8, cudaMemcpyDeviceToDevice, scat));
-        GCHECK(cudaEventRecord(ev_data[d], scat));
-    }
-    GCHECK(cudaEventRecord(t_up1, scat));
 
+    // ---- three host threads: this one issues the compute tasks; an uploader stages and
+    //      uploads the z chunks (a pageable caller's data through the bounce blocks, which
+    //      costs host memcpy time that must not hold up task issue); a downloader returns each
+    //      window's final planes as soon as its last pass is done. Tasks wait on a chunk's event
+    //      only after the uploader has recorded it (host-side handshake). ----
+    std::mutex mu;
+    std::condition_variable cv;
+    int chunks_done = 0, windows_issued = 0;
+    bool failed = false;
+    std::exception_ptr err_up, err_down;
+    auto mark_failed = [&] {
+        std::lock_guard<std::mutex> lk(mu);
+        failed = true;
+        cv.notify_all();
+    };
+    std::thread uploader([&] {
+        try {
+            GCHECK(cudaSetDevice(s.device));
+            for (int d = 0; d < nchunk; ++d) {
+                const int k0 = d * W, nk = std::min(W, h.Z - k0);
+                for (int c = 0; c < h.nc; ++c)
+                    upload_chunk(s.coeff(c, h.slab_elems(s)), v.coeffs[c], k0, nk);
+                upload_chunk(s.buf[b]->p, b == 0 ? v.u : v.v, k0, nk);
+                if (shell)
+                    upload_shell(k0, nk);
+                else
+                    upload_chunk(other, host_other, k0, nk);
+                for (int r = 1; r < 3 && !single; ++r)
+                    GCHECK(cudaMemcpyAsync(rot[r] + (size_t)k0 * pe, rot[0] + (size_t)k0 * pe,
+                                           size_t(nk) * pe * 8, cudaMemcpyDeviceToDevice, scat));
+                GCHECK(cudaEventRecord(ev_data[d], scat));
+                std::lock_guard<std::mutex> lk(mu);
+                chunks_done = d + 1;
+                cv.notify_all();
+            }
+            GCHECK(cudaEventRecord(t_up1, scat));
+        } catch (...) {
+            err_up = std::current_exception();
+            mark_failed();
+        }
+    });
     // ---- compute tasks, issued window by window (the order the inputs arrive in: a task that
     //      waits for late data never sits in a hardware queue ahead of a runnable one), each
     //      window's results downloaded right after its last pass; every awaited event is
@@ -1795,7 +1977,73 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     double* fin_b = single ? rot[0] : tail1 ? rot[(npass - 1) % 3] : rot[npass % 3];
     double* host_b = b == 0 ? v.u : v.v;
     double* host_o = b == 0 ? v.v : v.u;
-    for (int c = 0; c < nwin; ++c) {
+    struct Pending {
+        int slot;
+        double* host;
+        size_t bytes;
+    };
+    std::thread downloader([&] {
+        try {
+            GCHECK(cudaSetDevice(s.device));
+            std::deque<Pending> fifo;
+            int nslot = 0;
+            auto drain_one = [&] {
+                const Pending pd = fifo.front();
+                fifo.pop_front();
+                GCHECK(cudaEventSynchronize(ev_db[pd.slot]));
+                parallel_memcpy(pd.host, dbounce[pd.slot], pd.bytes);
+            };
+            for (int c = 0; c < nwin; ++c) {
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return windows_issued > c || failed; });
+                    if (windows_issued <= c) return;
+                }
+                const int lo = std::max(0, z0[c] - off[npass - 1]);
+                const int hi = std::min(h.nz, z0[c + 1] - off[npass - 1]);
+                if (hi <= lo) continue;
+                GCHECK(cudaStreamWaitEvent(down, ev_task[size_t(c) * npass + npass - 1], 0));
+                for (int f = 0; f < 2; ++f) {
+                    for (int k0 = h.R + lo; k0 < h.R + hi; k0 += W) {
+                        const int nk = std::min(W, h.R + hi - k0);
+                        const double* dsrc = (f == 0 ? fin_b : other) + (size_t)k0 * pe + h.off;
+                        double* hdst = (f == 0 ? host_b : host_o) + size_t(k0) * hplane;
+                        if (!dbounce) {
+                            GCHECK(cudaMemcpy2DAsync(hdst, size_t(plane_x) * 8, dsrc,
+                                                     size_t(h.pitch) * 8, size_t(plane_x) * 8,
+                                                     size_t(nk) * rows, cudaMemcpyDeviceToHost,
+                                                     down));
+                            continue;
+                        }
+                        if (int(fifo.size()) == NBD) drain_one();  // frees the oldest block
+                        const int j = nslot++ % NBD;
+                        GCHECK(cudaMemcpy2DAsync(dbounce[j], size_t(plane_x) * 8, dsrc,
+                                                 size_t(h.pitch) * 8, size_t(plane_x) * 8,
+                                                 size_t(nk) * rows, cudaMemcpyDeviceToHost, down));
+                        GCHECK(cudaEventRecord(ev_db[j], down));
+                        fifo.push_back({j, hdst, size_t(nk) * hplane * 8});
+                    }
+                }
+            }
+            while (!fifo.empty()) drain_one();
+            GCHECK(cudaEventRecord(t_dn1, down));
+        } catch (...) {
+            err_down = std::current_exception();
+            mark_failed();
+        }
+    });
+    struct Joiner {  // never leave a thread running (or waiting) when this one throws
+        std::thread* a;
+        std::thread* b;
+        std::function<void()> fail;
+        ~Joiner() {
+            if (a->joinable() || b->joinable()) fail();
+            if (a->joinable()) a->join();
+            if (b->joinable()) b->join();
+        }
+    } joiner{&uploader, &downloader, mark_failed};
+    bool aborted = false;  // the uploader failed: issue nothing more
+    for (int c = 0; c < nwin && !aborted; ++c) {
         cudaStream_t st = ws[c];
         for (int q = 0; q < npass; ++q) {
             const bool last = q == npass - 1;
@@ -1809,6 +2057,14 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
             const int lo = std::max(0, z0[c] - off[q]), hi = std::min(h.nz, z0[c + 1] - off[q]);
             if (q == 0) {  // inputs: planes up to the window top + H (+R allocated offset)
                 const int need = std::min(nchunk - 1, (z0[c + 1] + hp[0] * h.R + h.R) / W);
+                {
+                    std::unique_lock<std::mutex> lk(mu);  // the uploader has recorded it
+                    cv.wait(lk, [&] { return chunks_done > need || failed; });
+                    if (chunks_done <= need) {
+                        aborted = true;
+                        break;
+                    }
+                }
                 GCHECK(cudaStreamWaitEvent(st, ev_data[need], 0));
             } else if (c > 0) {
                 GCHECK(cudaStreamWaitEvent(st, ev_task[size_t(c - 1) * npass + (q - 1)], 0));
@@ -1829,28 +2085,22 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                 p.dst_penult = pen;
                 p.work = reinterpret_cast<int*>(counters->p) + size_t(c) * npass + q;
                 p.work_base = 0;
-                const CUtensorMap& omap = tensor_map(h, 0, dst, 1, p.ox, var->ly - 2 * tb * h.R, 1);
-                GCHECK(var->launch(vmap, cmap, umap, omap, p, li.grid, st));
+                const PassDesc pd = single_desc(h, 0, var, tb, p, vmap, umap);
+                GCHECK(var->launch(cmap, pd, p, li.grid, st));
                 computed += li.computed_lups;
                 ++launches;
             }
             GCHECK(cudaEventRecord(ev_task[size_t(c) * npass + q], st));
         }
-        // this window's final planes go back as soon as its last pass is done
-        const int lo = std::max(0, z0[c] - off[npass - 1]);
-        const int hi = std::min(h.nz, z0[c + 1] - off[npass - 1]);
-        if (hi <= lo) continue;
-        GCHECK(cudaStreamWaitEvent(down, ev_task[size_t(c) * npass + npass - 1], 0));
-        const int k0 = h.R + lo, nk = hi - lo;
-        for (int f = 0; f < 2; ++f) {
-            const double* dsrc = (f == 0 ? fin_b : other) + (size_t)k0 * pe + h.off;
-            double* hdst = (f == 0 ? host_b : host_o) + size_t(k0) * hplane;
-            GCHECK(cudaMemcpy2DAsync(hdst, size_t(plane_x) * 8, dsrc, size_t(h.pitch) * 8,
-                                     size_t(plane_x) * 8, size_t(nk) * rows,
-                                     cudaMemcpyDeviceToHost, down));
-        }
+        if (aborted) break;
+        std::lock_guard<std::mutex> lk(mu);  // its last-pass event is recorded
+        windows_issued = c + 1;
+        cv.notify_all();
     }
-    GCHECK(cudaEventRecord(t_dn1, down));
+    uploader.join();
+    downloader.join();
+    if (err_up) std::rethrow_exception(err_up);
+    if (err_down) std::rethrow_exception(err_down);
     GCHECK(cudaEventSynchronize(t_dn1));
     for (auto q : ws) GCHECK(cudaStreamSynchronize(q));
     if (std::getenv("GIRIH_STREAM_TRACE")) {  // diagnostics: when each window's passes ran
@@ -1907,6 +2157,17 @@ double step_timed(Handle& h, long long steps, girih_gpu_report* rep) {
         GCHECK(cudaEventRecord(e1[g], h.slabs[g].stream));
     }
     sync_all(h);
+    // the chained kernel's dependency watchdog (zwave.cuh) flags a wait that never ended
+    for (Slab& s : h.slabs) {
+        int flag = 0;
+        GCHECK(cudaSetDevice(s.device));
+        GCHECK(cudaMemcpy(&flag, reinterpret_cast<int*>(s.work->p) + 1, sizeof flag,
+                          cudaMemcpyDeviceToHost));
+        if (flag) {
+            GCHECK(cudaMemset(reinterpret_cast<int*>(s.work->p) + 1, 0, sizeof flag));
+            throw_err(GIRIH_ECUDA, "chained pass dependency wait timed out (results invalid)");
+        }
+    }
     double ksec = 0;
     for (size_t g = 0; g < h.slabs.size(); ++g) {
         float ms = 0;
@@ -1993,6 +2254,8 @@ int girih_gpu_variant_info(int index, girih_gpu_variant* out) {
         out->threads = v->threads;
         out->prefetch = v->prefetch;
         out->smem_bytes = v->smem_bytes;
+        out->cluster_y = v->cy;
+        out->aux_prefetch = v->aux_prefetch;
     });
 }
 
@@ -2226,6 +2489,38 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
     });
 }
 
+int girih_gpu_row_digest(void* handle, int field, unsigned long long* digest) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (!digest) throw_err(GIRIH_EINVAL, "null argument");
+        if (field < 0 || field >= 2 + h.nc) throw_err(GIRIH_EINVAL, "no such field");
+        // row hashes of every allocated row in (k, j) order, each slab hashing the planes it is
+        // authoritative for; the fold over them (8 bytes per row) runs on the host
+        std::vector<unsigned long long> rows((size_t)h.Z * h.Y);
+        for (Slab& s : h.slabs) {
+            int k0, k1;
+            auth_planes(h, s, &k0, &k1);
+            if (k1 <= k0) continue;
+            GCHECK(cudaSetDevice(s.device));
+            const double* dev = field < 2 ? s.buf[field]->p : s.coeff(field - 2, h.slab_elems(s));
+            DevBuf out;
+            out.alloc(s.device, size_t(k1 - k0) * h.Y * 8);
+            auto* o = reinterpret_cast<unsigned long long*>(out.p);
+            GCHECK(launch_row_fnv(dev, h.pitch, h.off, h.X, h.Y, k0 - s.zoff, k1 - k0, o, s.stream));
+            GCHECK(cudaMemcpyAsync(rows.data() + size_t(k0) * h.Y, o, size_t(k1 - k0) * h.Y * 8,
+                                   cudaMemcpyDeviceToHost, s.stream));
+            GCHECK(cudaStreamSynchronize(s.stream));
+        }
+        unsigned long long d = 0xCBF29CE484222325ull;
+        for (unsigned long long r : rows)
+            for (int b = 0; b < 8; ++b) {
+                d ^= (r >> (8 * b)) & 0xFFull;
+                d *= 0x100000001B3ull;
+            }
+        *digest = d;
+    });
+}
+
 int girih_gpu_download_coeffs(void* handle, double* const* coeffs, int n, double* cc) {
     return guarded([&] {
         Handle& h = *as_handle(handle);
@@ -2368,6 +2663,12 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
     return guarded([&] {
         Handle& h = *as_handle(handle);
         if (!best) throw_err(GIRIH_EINVAL, "null argument");
+        // a multi-process slab handle cannot tune alone: its passes wait on (IPC) or exchange
+        // with (NCCL) its neighbours, and timing-driven searches would diverge across ranks.
+        // Tune a single-GPU handle on one rank and hand the result to every rank instead.
+        if (h.nranks > 1 || h.ipc)
+            throw_err(GIRIH_ESTATE, "girih_gpu_tune needs a single-process handle (tune one rank "
+                                    "on a single-GPU state and broadcast the config)");
         const int tb_cap = std::max(1, std::min(max_tb_req > 0 ? max_tb_req : 64, max_tb(h.kind)));
         // snapshot the solution fields so tuning leaves the state untouched (the reference
         // tunes on scratch state, make_engine_measure, proj/src/tuner.cpp:212-223)

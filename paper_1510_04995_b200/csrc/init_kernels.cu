@@ -88,6 +88,36 @@ cudaError_t launch_compare_field(const double* dev, int pitch, int off, int X, i
     return cudaGetLastError();
 }
 
+// ---- row digest: FNV-1a (64-bit) of the bytes of each allocated row (k, j) of local planes
+// [k0, k0 + nk), i.e. the X elements at device offset `off`, in host order. One thread per row;
+// the host folds the row hashes (girih_gpu_row_digest). ----
+__global__ void row_fnv_kernel(const double* __restrict__ dev, int pitch, int off, int X, int Y,
+                               int k0, int nk, unsigned long long* __restrict__ out) {
+    const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (r >= static_cast<long long>(nk) * Y) return;
+    const int k = static_cast<int>(r / Y), j = static_cast<int>(r % Y);
+    const double* row = dev + (static_cast<long long>(k0 + k) * Y + j) * pitch + off;
+    unsigned long long h = 0xCBF29CE484222325ull;
+    for (int i = 0; i < X; ++i) {
+        const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(row[i]));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            h ^= (b >> (8 * q)) & 0xFFull;
+            h *= 0x100000001B3ull;
+        }
+    }
+    out[r] = h;
+}
+
+cudaError_t launch_row_fnv(const double* dev, int pitch, int off, int X, int Y, int k0, int nk,
+                           unsigned long long* out, cudaStream_t stream) {
+    const long long rows = static_cast<long long>(nk) * Y;
+    const int block = 128;
+    row_fnv_kernel<<<static_cast<unsigned>((rows + block - 1) / block), block, 0, stream>>>(
+        dev, pitch, off, X, Y, k0, nk, out);
+    return cudaGetLastError();
+}
+
 // ---- ghost shell of a field: scatter a packed [plane][shell] block into the device layout ----
 // Allocated planes [k0, k0 + nk) of a field whose interior is not needed (the input level t0-1
 // of a Jacobi run: overwritten before any read): ghost planes in full, in the other planes the

@@ -8,20 +8,20 @@
 
 namespace girih_gpu {
 
-using LaunchFn = cudaError_t (*)(const CUtensorMap& vmap, const CUtensorMap& cmap,
-                                 const CUtensorMap& umap, const CUtensorMap& omap,
-                                 const PassParams& p, int grid, cudaStream_t stream);
+using LaunchFn = cudaError_t (*)(const CUtensorMap& cmap, const PassDesc& d, const PassParams& p,
+                                 int grid, cudaStream_t stream);
 using LaunchChainFn = cudaError_t (*)(const CUtensorMap& cmap, const ChainDescs& cd,
                                       const PassParams& p, int grid, cudaStream_t stream);
-using OccFn = cudaError_t (*)(int* blocks_per_sm);
+using OccFn = cudaError_t (*)(int* max_ctas);  // resident CTAs on the whole current device
 
 struct Variant {
     int kind, tb, lx, ly, threads, prefetch, aux_prefetch, min_blocks;
+    int cy;                      // CTAs per thread-block cluster along y (1 = no cluster)
     int smem_bytes;
     int aux_x0, aux_y0, aux_x, aux_y;  // coefficient (aux) box inside the tile
     LaunchFn launch;             // one pass
-    LaunchChainFn launch_chain;  // cd.npass chained passes over the same tile grid
-    OccFn occupancy;             // resident CTAs per SM, single-pass kernel
+    LaunchChainFn launch_chain;  // cd.npass chained passes over the same tile grid (cy == 1)
+    OccFn occupancy;             // resident CTAs, single-pass kernel (a multiple of cy)
     OccFn occupancy_chain;       // the same for the chained kernel
 };
 
@@ -35,64 +35,121 @@ extern const int kNumVariantsConst25;
 extern const Variant kVariantsVar25[];
 extern const int kNumVariantsVar25;
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY>
 cudaError_t launch_zwave_impl(const CUtensorMap& cmap, const ChainDescs& cd, const PassParams& p,
                               int grid, cudaStream_t stream) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY>;
     // once per instantiation (thread-safe static initialisation)
     static const cudaError_t attr =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
     if (attr != cudaSuccess) return attr;
-    fn<<<grid, NT, CFG::SMEM, stream>>>(cmap, cd, p);
+    if constexpr (CY == 1) {
+        fn<<<grid, NT, CFG::SMEM, stream>>>(cmap, cd, p);
+    } else {
+        if constexpr (CY > 8) {
+            static const cudaError_t np =
+                cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (np != cudaSuccess) return np;
+        }
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(unsigned(grid / CY * CY));
+        lc.blockDim = dim3(NT);
+        lc.dynamicSmemBytes = CFG::SMEM;
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CY;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&lc, fn, cmap, cd, p);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY>
 cudaError_t launch_zwave_chain(const CUtensorMap& cmap, const ChainDescs& cd, const PassParams& p,
                                int grid, cudaStream_t stream) {
-    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, true>(cmap, cd, p, grid, stream);
+    if constexpr (CY > 1) {
+        return cudaErrorNotSupported;  // cluster kernels run single passes
+    } else {
+        return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, true, 1>(cmap, cd, p, grid, stream);
+    }
 }
 
 // one pass = a chain of length 1 (no dependency flags)
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB>
-cudaError_t launch_zwave(const CUtensorMap& vmap, const CUtensorMap& cmap, const CUtensorMap& umap,
-                         const CUtensorMap& omap, const PassParams& p, int grid,
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY>
+cudaError_t launch_zwave(const CUtensorMap& cmap, const PassDesc& d, const PassParams& p, int grid,
                          cudaStream_t stream) {
     ChainDescs cd{};
-    cd.d[0].vmap = vmap;
-    cd.d[0].umap = umap;
-    cd.d[0].omap = omap;
-    cd.d[0].dst_final = p.dst_final;
-    cd.d[0].dst_penult = p.dst_penult;
-    cd.d[0].parity0 = p.parity0;
+    cd.d[0] = d;
     cd.pidx[0] = 0;
     cd.npass = 1;
     cd.done = nullptr;
-    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false>(cmap, cd, p, grid, stream);
+    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false, CY>(cmap, cd, p, grid, stream);
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN = false>
-cudaError_t occupancy_zwave(int* blocks) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN>;
-    cudaError_t e =
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, NT, CFG::SMEM);
-}
-
-#define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB)                                        \
-    Variant {                                                                                 \
-        KIND, TB, LX, LY, NT, P, PA, MINB, int(ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::SMEM),     \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AXO,                                    \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AYO,                                    \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AX,                                     \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>::AY,                                     \
-            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>,                                       \
-            &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB>,                                 \
-            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB>,                                    \
-            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, true>                               \
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY, bool CHAIN = false>
+cudaError_t occupancy_zwave(int* max_ctas) {
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
+    *max_ctas = 0;
+    if constexpr (CHAIN && CY > 1) {
+        return cudaSuccess;  // not launchable chained
+    } else {
+        auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY>;
+        cudaError_t e =
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+            return e;
+        if constexpr (CY == 1) {
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, CFG::SMEM);
+            *max_ctas = per_sm * sms;
+            return e;
+        } else {
+            if constexpr (CY > 8) {
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e != cudaSuccess) return e;
+            }
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(unsigned(CY * sms));
+            lc.blockDim = dim3(NT);
+            lc.dynamicSmemBytes = CFG::SMEM;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CY;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int clusters = 0;
+            e = cudaOccupancyMaxActiveClusters(&clusters, fn, &lc);
+            *max_ctas = clusters * CY;
+            return e;
+        }
     }
+}
+
+#define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY)                                \
+    Variant {                                                                                 \
+        KIND, TB, LX, LY, NT, P, PA, MINB, CY,                                                \
+            int(ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::SMEM),                    \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AXO,                          \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AYO,                          \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AX,                           \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AY,                           \
+            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                             \
+            &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                       \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                          \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY, true>                     \
+    }
+#define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB) \
+    GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, 1)
 
 }  // namespace girih_gpu

@@ -12,6 +12,8 @@ const Variant kVariantsConst25[] = {
     GIRIH_VARIANT(K_CONST25, 1, 64, 20, 128, 1, 1, 2),
     GIRIH_VARIANT(K_CONST25, 1, 64, 20, 128, 2, 1, 2),
     GIRIH_VARIANT(K_CONST25, 2, 32, 32, 192, 2, 1, 1),
+    GIRIH_VARIANT_C(K_CONST25, 2, 64, 20, 192, 1, 1, 1, 4),
+    GIRIH_VARIANT_C(K_CONST25, 2, 64, 16, 128, 1, 1, 1, 8),
 };
 const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
 

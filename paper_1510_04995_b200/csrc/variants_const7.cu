@@ -12,6 +12,9 @@ const Variant kVariantsConst7[] = {
     GIRIH_VARIANT(K_CONST7, 2, 64, 34, 512, 4, 0, 1),
     GIRIH_VARIANT(K_CONST7, 3, 64, 32, 480, 3, 0, 1),
     GIRIH_VARIANT(K_CONST7, 4, 64, 32, 480, 2, 0, 1),
+    GIRIH_VARIANT_C(K_CONST7, 2, 64, 18, 256, 3, 0, 2, 4),
+    GIRIH_VARIANT_C(K_CONST7, 3, 64, 32, 480, 3, 0, 1, 4),
+    GIRIH_VARIANT_C(K_CONST7, 4, 64, 32, 480, 2, 0, 1, 4),
 };
 const int kNumVariantsConst7 = sizeof(kVariantsConst7) / sizeof(kVariantsConst7[0]);
 

@@ -18,6 +18,13 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT(K_VAR7, 2, 32, 16, 224, 2, 2, 2),
     GIRIH_VARIANT(K_VAR7, 3, 32, 16, 224, 3, 1, 1),
     GIRIH_VARIANT(K_VAR7, 4, 32, 16, 224, 2, 1, 1),
+    GIRIH_VARIANT_C(K_VAR7, 2, 64, 18, 512, 2, 1, 1, 2),
+    GIRIH_VARIANT_C(K_VAR7, 2, 64, 18, 512, 2, 1, 1, 4),
+    GIRIH_VARIANT_C(K_VAR7, 3, 64, 12, 320, 2, 1, 1, 4),
+    GIRIH_VARIANT_C(K_VAR7, 3, 64, 12, 160, 2, 1, 1, 4),
+    GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 256, 2, 1, 1, 4),
+    GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 256, 2, 1, 1, 8),
+    GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 128, 2, 1, 1, 4),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

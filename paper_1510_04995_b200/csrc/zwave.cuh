@@ -123,7 +123,8 @@ constexpr int CHAIN_MAX = 128;  // passes in one launch
 struct PassDesc {               // what changes from pass to pass
     CUtensorMap vmap;           // level-0 source buffer (3-D)
     CUtensorMap umap;           // const25pt: level t0-1 (3-D)
-    CUtensorMap omap;           // output: interior of dst_final
+    CUtensorMap omap;           // output: interior of dst_final (cluster: its outer CTAs)
+    CUtensorMap omap_in;        // cluster kernels: output map of the inner CTAs (taller box)
     double* dst_final;          // level t0+TB (odd-nx last column stored directly)
     double* dst_penult;         // level t0+TB-1 or nullptr
     int parity0;                // parity of t0
@@ -212,6 +213,36 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// thread-block clusters (y-neighbour CTAs share the halo rows of the fused levels through
+// distributed shared memory)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+#ifndef GIRIH_CLUSTER_NOSYNC
+#define GIRIH_CLUSTER_NOSYNC 0  // timing experiment only: no per-iteration cluster barrier
+#endif
+// shared::cta address -> the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_d2(uint32_t addr, double2 v) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cluster_s32(uint32_t addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -266,13 +297,26 @@ __device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int t
     }
 }
 
-// advance within / across units; the drawing cursor (V producer) fetches new unit ids
-template <int H, bool CHAIN, bool DRAW>
+// advance within / across units; the drawing cursor (V producer) fetches new unit ids.
+// Clusters (CY > 1): the CTAs of a cluster work on the same unit (tile column, z chunk); only
+// the leader CTA's producer draws, and it publishes every id into all the cluster's unit queues
+// a whole unit before anyone needs it (the cluster barrier of every iteration orders the remote
+// stores before the reads).
+template <int H, bool CHAIN, bool DRAW, int CY = 1>
 __device__ __forceinline__ void cursor_next(Cursor& c, const PassParams& p, int total,
                                             volatile int* uq, int* drawn) {
     if (++c.it >= c.n_it) {
         int next;
-        if (DRAW) {
+        if (DRAW && CY > 1) {
+            next = uq[(c.seq + 1) % UQ];  // published when this cursor entered unit seq
+            if (next < total) {
+                const int d = int(gridDim.x) / CY + atomicAdd(p.work, 1) - p.work_base;
+                const int v = d < total ? d : total;
+                const uint32_t a = smem_u32(const_cast<int*>(&uq[(c.seq + 2) % UQ]));
+#pragma unroll
+                for (int r = 0; r < CY; ++r) st_cluster_s32(mapa_rank(a, r), v);
+            }
+        } else if (DRAW) {
             // the id drawn at the start of this unit; draw the one after it now, so the atomic's
             // latency hides behind a whole unit instead of stalling the producer warp
             next = *drawn;
@@ -344,7 +388,7 @@ template <> struct AuxArrays<K_CONST25> { static constexpr int N = 2; };  // C a
 
 constexpr int round16(int n) { return (n + 15) / 16 * 16; }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1, int CY = 1>
 struct ZwaveConfig {
     static constexpr int R = KindTraits<KIND>::R;
     static constexpr int Q = 2 * R + 1;     // z window of one level
@@ -355,6 +399,16 @@ struct ZwaveConfig {
     static constexpr int NR0 = R + 1 + P;   // level-0 TMA ring depth
     static constexpr int H = TB * R;        // halo of the loaded tile
     static constexpr int OY = LY - 2 * H;   // output tile height (x: runtime, halo H or H+1)
+    // Thread-block clusters of CY CTAs stacked along y (CY > 1, TB >= 2). CTA c's box starts
+    // c*OWN rows above CTA c-1's, so neighbouring boxes overlap by the 2R level-0 rows each
+    // needs from the other. Every CTA computes its OWN rows [R, LY-R) at every level; the rows
+    // of level s-1 beyond an INNER edge are the neighbour's own rows, which it pushes into this
+    // CTA's ring through distributed shared memory. Only the cluster's outer edges keep the
+    // trapezoid halo, so the redundant rows per CTA drop from 2(TB-1)R to 2(TB-1)R/CY.
+    static constexpr int OWN = LY - 2 * R;
+    static constexpr int OYS = CY > 1 ? OWN : OY;                 // widest output rows of a CTA
+    static constexpr int OYC = CY > 1 ? CY * OWN - 2 * (TB - 1) * R : OY;  // per cluster
+    static constexpr int OYE = CY > 1 ? LY - R - H : OY;          // outer CTAs' output rows
     static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
     // threads cover the level-1 valid rows [R, LY - R) only: the R outermost rows of the
@@ -380,7 +434,7 @@ struct ZwaveConfig {
     static constexpr int AUXPLANE = NAUX * AYX;
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
     static constexpr int GUARD = round16(LX * R + R + 8);
-    static constexpr int STAGE = round16(OXM * OY);  // one output staging plane
+    static constexpr int STAGE = round16(OXM * OYS);  // one output staging plane
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
                                            size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
@@ -388,24 +442,28 @@ struct ZwaveConfig {
     static_assert(NT % 32 == 0, "whole warps");
     static_assert(!STACK || CR % (NT / 32) == 0, "STACK: every warp owns whole rows");
     static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
-    static_assert(LX - 2 * H - 2 > 0 && OY > 0, "tile too small for the halo (x halo may be H+1)");
+    static_assert(LX - 2 * H - 2 > 0 && OYE > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
     static_assert((LX * 8) % 16 == 0 && (AX * 8) % 16 == 0, "TMA inner box must be 16-byte multiple");
     static_assert((CELLS * 8) % 128 == 0 && (AYX * 8) % 128 == 0, "TMA smem boxes 128-byte aligned");
     static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
+    static_assert(CY == 1 || (TB >= 2 && OYE > 0 && OWN >= 2 * R && CY <= 16),
+                  "clusters share fused-level halo rows: TB >= 2, outer CTAs need output rows");
 };
 
 // CHAIN = false: one pass (descriptors d[0]); true: cd.npass chained passes. The two are
 // separate instantiations so that single-pass launches carry none of the chaining state (the
 // 128-register var7pt CTA spills otherwise, and shared-memory producer state cost 30%).
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY = 1>
 __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 1) ? MINB - 1 : MINB)
     zwave_kernel(const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
                  const __grid_constant__ ChainDescs cd,     // per-pass buffers and maps
                  const __grid_constant__ PassParams p) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
+    static_assert(CY == 1 || !CHAIN, "cluster kernels run single passes");
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
-    constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA, OY = CFG::OY;
+    constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA;
+    constexpr int OWN = CFG::OWN, OYC = CFG::OYC;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr bool CQ = CFG::CQ;
     // x neighbours by warp shuffle (misaligned pair loads cost two shared-memory wavefronts
@@ -424,11 +482,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     double* ring0 = reinterpret_cast<double*>(smem_raw) + GUARD;
     double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*QL*CELLS
     double* auxr = ringL + (TB - 1) * QL * CELLS;  // aux planes: NAR x [NAUX][AY][AX]
-    double* stage = auxr + NAR * AUXPLANE + GUARD; // 3 output staging planes [OY][ox]
+    double* stage = auxr + NAR * AUXPLANE + GUARD; // 3 output staging planes [OYS][ox]
     uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 3 * STAGE);
     uint64_t* abar = vbar + NR0;
 
     const int tid = threadIdx.x;
+    // cluster position (CY > 1): rank c owns box rows [R, LY-R) of the cluster tile's c-th box;
+    // the outer CTAs (c = 0, CY-1) keep the trapezoid halo on their outer side
+    const int crank = CY > 1 ? int(cluster_ctarank()) : 0;
+    const bool lo_edge = crank == 0, hi_edge = crank == CY - 1;
+    const int oy_lo = lo_edge ? H : R;  // first output row of this CTA's box
     if (tid == 0) {
         for (int b = 0; b < NR0; ++b) mbar_init(&vbar[b], 1);
         for (int b = 0; b < NAR; ++b) mbar_init(&abar[b], 1);
@@ -458,10 +521,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     // the consumer needs this plane now. If this CTA's own last unit is a
                     // dependency, the store thread publishes it at the top of this same
                     // iteration (before the barrier this thread is held at), so the wait ends.
+                    // watchdog (~2 minutes): a wait that long is a bug; flag it for the host
+                    // (girih_gpu_step then fails with GIRIH_ECUDA) and proceed rather than hang
+                    // the GPU or kill the context with a trap
                     long long spins = 0;
                     while (!chain_deps_ready(p, cd.done, vcur.q, ul)) {
                         __nanosleep(128);
-                        if (++spins > (1ll << 25)) __trap();  // never hang the GPU on a bug
+                        if (++spins > (1ll << 30)) {
+                            atomicExch(p.work + 1, 1);
+                            break;
+                        }
                     }
                 }
                 chain_acquire();
@@ -471,12 +540,15 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         const int j = vcur.ug.za - H + vcur.it;
         const int slot = int(vnext % NR0);
         const int xd = p.off + vcur.ug.tx * p.ox + R - p.hx;  // even by construction
-        const int yd = vcur.ug.ty * OY + R - H;
+        const int yd = vcur.ug.ty * OYC + crank * OWN + R - H;
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
         tma_load_plane(ring0 + slot * CELLS, &cd.d[CHAIN ? cd.pidx[vcur.q] : 0].vmap, xd, yd, j,
                        &vbar[slot]);
         ++vnext;
-        cursor_next<H, CHAIN, true>(vcur, p, total, uq, &drawn);
+        if (CY > 1 && crank > 0)  // cluster members replay the leader's units
+            cursor_next<H, CHAIN, false>(vcur, p, total, uq, nullptr);
+        else
+            cursor_next<H, CHAIN, true, CY>(vcur, p, total, uq, &drawn);
         if (CHAIN && vcur.it == 0) vready = false;
         return true;
     };
@@ -486,7 +558,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             const int k1 = acur.ug.za - H + acur.it - R;  // level-1 plane of that iteration
             const int slot = int(anext % NAR);
             const int xd = p.off + acur.ug.tx * p.ox + R - p.hx + AXO;
-            const int yd = acur.ug.ty * OY + R - H + AYO;
+            const int yd = acur.ug.ty * OYC + crank * OWN + R - H + AYO;
             if (acur.it < 2 * R) {
                 // no level reads the aux plane of the first 2R iterations of a unit: complete
                 // the phase without moving data
@@ -509,7 +581,36 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         }
     };
     static_assert(P >= PA, "the V producer draws units and must lead the aux producer");
-    if (tid == 0) {
+    if constexpr (CY > 1) {
+        // the leader hands out the cluster's first two units (cluster c starts with unit c),
+        // once every CTA of the cluster is running (distributed shared memory is only valid then)
+        cluster_arrive();
+        cluster_wait();
+        if (tid == 0 && crank == 0) {
+            const int ncl = int(gridDim.x) / CY, cid = int(blockIdx.x) / CY;
+            const int u0 = cid < total ? cid : total;
+            int u1 = total;
+            if (u0 < total) {
+                const int d = ncl + atomicAdd(p.work, 1) - p.work_base;
+                u1 = d < total ? d : total;
+            }
+#pragma unroll
+            for (int r = 0; r < CY; ++r) {
+                st_cluster_s32(mapa_rank(smem_u32(&uq[0]), r), u0);
+                st_cluster_s32(mapa_rank(smem_u32(&uq[1]), r), u1);
+            }
+        }
+        cluster_arrive();  // the queues (and every CTA's mbarriers) are initialised
+        cluster_wait();
+        if (tid == 0) {
+            const int u0 = reinterpret_cast<volatile int*>(uq)[0];
+            cursor_set<H, CHAIN>(vcur, p, total, 0, u0);
+            cursor_set<H, CHAIN>(acur, p, total, 0, u0);
+            for (int e = 0; e < P; ++e) issue_v(true);
+            for (int e = 0; e < PA; ++e) issue_a();
+        }
+        cluster_arrive();  // pairs with the first iteration's wait
+    } else if (tid == 0) {
         // single-pass launches: the first unit is blockIdx.x. Chained launches draw it too, so
         // that every unit another CTA may wait for belongs to a CTA that is already running
         // (drawing takes residency; launch order alone would not guarantee it).
@@ -555,7 +656,10 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                                  : 2 * (tid + NT * i) + R * LX;
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
-        const int dy = min(ly, LY - 1 - ly);
+        // distance to the nearest box edge that has a trapezoid halo (inner cluster edges have
+        // none: the neighbour supplies the rows beyond them)
+        const int dy = min((CY > 1 && !lo_edge) ? 1 << 20 : ly,
+                           (CY > 1 && !hi_edge) ? 1 << 20 : LY - 1 - ly);
         dyv[i] = dy;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -563,7 +667,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             if (dx >= p.hx && dy >= H) out_mask |= 1u << (2 * i + q);
         }
         ai[i] = (ly - AYO) * AX + (lx - AXO);
-        sidx[i] = (ly - H) * p.ox + (lx - p.hx);
+        sidx[i] = (ly - oy_lo) * p.ox + (lx - p.hx);
     }
     // pairs whose whole warp lies outside the level-s valid rows skip the stencil (warp-uniform;
     // their values are never read): bit (s-1)*PPT + i. Only for R = 1: the 25-point bodies are
@@ -632,7 +736,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         }
         const int n_it = (ug.zb - ug.za) + 2 * H;
         const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
-        const int ya0 = ug.ty * OY + R - H;
+        const int ya0 = ug.ty * OYC + crank * OWN + R - H;
 
         // ghost columns (ghost value instead of the stencil) and in-allocation columns
         uint32_t ghost_mask = 0, ok_mask = 0, odd_mask = 0;
@@ -672,8 +776,9 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             if (tid == STORE_TID) {
                 stored_now = false;
                 if (pend) {  // output plane of the previous iteration (staging fenced by writers)
-                    tma_store_plane(&cd.d[CHAIN ? cd.pidx[pend_q] : 0].omap, stage + pend_b * STAGE,
-                                    pend_x, pend_y, pend_z);
+                    const PassDesc& od = cd.d[CHAIN ? cd.pidx[pend_q] : 0];
+                    tma_store_plane((CY > 1 && !lo_edge && !hi_edge) ? &od.omap_in : &od.omap,
+                                    stage + pend_b * STAGE, pend_x, pend_y, pend_z);
                     bulk_commit();
                     pend = false;
                     stored_now = true;
@@ -753,8 +858,18 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             int ring_slot[TB];  // centre-ring slot each level writes this iteration (-1: none)
 #pragma unroll
             for (int L = 0; L < TB; ++L) ring_slot[L] = -1;
+            // clusters: levels >= 2 read halo rows the neighbour CTAs pushed at the end of an
+            // earlier iteration; the wait sits after level 1 so the barrier's latency hides
+            // behind it (the arrive is at the end of the previous iteration)
+            [[maybe_unused]] bool cwaited = false;
 #pragma unroll
             for (int s = 1; s <= TB; ++s) {
+                if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC) {
+                    if (s == 2) {
+                        cluster_wait();
+                        cwaited = true;
+                    }
+                }
                 const int k = j - s * R;  // plane of level s
                 // lower bounds are monotone in s (higher levels sit on lower planes)
                 if (it < 2 * s * R || k < 0) break;
@@ -1000,6 +1115,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     staged = true;
                 }
             }
+            if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC)
+                if (!cwaited) cluster_wait();
             // deferred centre-ring stores of levels 1..TB-1 (read by other threads from the
             // next iteration on, behind the barrier)
 #pragma unroll
@@ -1008,7 +1125,23 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 double2* wr = reinterpret_cast<double2*>(ringL + ((L - 1) * QL + ring_slot[L]) * CELLS);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) wr[lcell[i] >> 1] = fresh[L][i];
+                if constexpr (CY > 1) {
+                    // the R own rows next to an inner edge also go into the neighbour's ring,
+                    // as the rows beyond its edge (same slot and column, row shifted by OWN)
+#pragma unroll
+                    for (int i = 0; i < PPT; ++i) {
+                        const int ly = lcell[i] / LX;
+                        if (!lo_edge && ly < 2 * R)
+                            st_cluster_d2(mapa_rank(smem_u32(&wr[(lcell[i] + OWN * LX) >> 1]), crank - 1),
+                                          fresh[L][i]);
+                        if (!hi_edge && ly >= LY - 2 * R)
+                            st_cluster_d2(mapa_rank(smem_u32(&wr[(lcell[i] - OWN * LX) >> 1]), crank + 1),
+                                          fresh[L][i]);
+                    }
+                }
             }
+            if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC)
+                cluster_arrive();  // this iteration's ring rows are complete
             // advance every level's z queue by one plane (and the coefficient queue)
             if constexpr (CQ) {
 #pragma unroll
@@ -1043,7 +1176,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 if (tid == STORE_TID) {
                     pend = true;
                     pend_x = ug.tx * p.ox;
-                    pend_y = ug.ty * OY;
+                    pend_y = ug.ty * OYC + crank * OWN + oy_lo - H;
                     pend_z = j - H - p.oz0;
                     pend_b = int(g % 3);
                     if constexpr (CHAIN) pend_q = uflags >> 1;
@@ -1072,11 +1205,13 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             unroll_phases<0, NPH>(phase);
         }
     }
+    if constexpr (CY > 1) cluster_wait();  // no CTA leaves while a neighbour may push into it
     __syncthreads();
     if (tid == STORE_TID) {
         if (pend) {
-            tma_store_plane(&cd.d[CHAIN ? cd.pidx[pend_q] : 0].omap, stage + pend_b * STAGE, pend_x,
-                            pend_y, pend_z);
+            const PassDesc& od = cd.d[CHAIN ? cd.pidx[pend_q] : 0];
+            tma_store_plane((CY > 1 && !lo_edge && !hi_edge) ? &od.omap_in : &od.omap,
+                            stage + pend_b * STAGE, pend_x, pend_y, pend_z);
             bulk_commit();
         }
         bulk_wait_all();

@@ -152,7 +152,8 @@ def variants():
         v = GirihGpuVariant()
         check(lib.girih_gpu_variant_info(i, C.byref(v)))
         out.append(dict(index=i, kind=v.kind, tb=v.tb, lx=v.lx, ly=v.ly, threads=v.threads,
-                        prefetch=v.prefetch, smem_bytes=v.smem_bytes))
+                        prefetch=v.prefetch, smem_bytes=v.smem_bytes, cluster_y=v.cluster_y,
+                        aux_prefetch=v.aux_prefetch))
     return out
 
 
@@ -374,6 +375,14 @@ class DeviceState:
         k, rem = divmod(first.value, arr.shape[1] * arr.shape[2])
         j, i = divmod(rem, arr.shape[2])
         return n.value, (i, j, k)
+
+    def row_digest(self, field) -> int:
+        """Device-side digest of a whole field ('u', 'v' or coefficient index c), ghosts and pad
+        included: FNV-1a over the per-row FNV-1a hashes (girih_gpu_row_digest)."""
+        f = {"u": 0, "v": 1}[field] if isinstance(field, str) else 2 + int(field)
+        d = C.c_ulonglong()
+        check(load().girih_gpu_row_digest(self._handle(), f, C.byref(d)))
+        return d.value
 
     def upload(self, state: ProblemState) -> None:
         v = _View(state)

@@ -97,6 +97,8 @@ class Oracle:
         L.orc_interior_checksum.argtypes = [_dp] + [C.c_int] * 5
         L.orc_fnv_all.restype = C.c_uint64
         L.orc_fnv_all.argtypes = [_dp, C.c_uint64]
+        L.orc_row_digest.restype = C.c_uint64
+        L.orc_row_digest.argtypes = [_dp, C.c_uint64, C.c_uint64]
         self.L = L
 
     def init_value(self, seed, field_id, k, j, i) -> float:
@@ -136,6 +138,11 @@ class Oracle:
     def interior_checksum(self, s: HostState) -> int:
         return self.L.orc_interior_checksum(_ptr(s.current()), s.nx, s.ny, s.nz, s.pad_x,
                                             s.radius)
+
+    def row_digest(self, a: np.ndarray) -> int:
+        """FNV-1a over the per-row FNV-1a hashes of a [Z][Y][X] field (girih_gpu_row_digest)."""
+        assert a.dtype == np.float64 and a.flags.c_contiguous and a.ndim == 3
+        return self.L.orc_row_digest(_ptr(a), a.shape[0] * a.shape[1], a.shape[2])
 
     def fnv_all(self, a: np.ndarray) -> int:
         a = np.ascontiguousarray(a)

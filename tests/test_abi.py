@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(girih):
 
 
 def test_abi_version(girih):
-    assert girih.load().girih_gpu_abi_version() == 2
+    assert girih.load().girih_gpu_abi_version() == 3
 
 
 def test_traits_and_names(girih):
@@ -50,7 +50,12 @@ def test_variants_registry(girih):
         R = 1 if v["kind"] < 2 else 4
         # threads cover the level-1 rows [R, ly - R) in x-pairs
         assert v["lx"] * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
-        assert v["lx"] > 2 * R * v["tb"] and v["ly"] > 2 * R * v["tb"]
+        assert v["lx"] > 2 * R * v["tb"]
+        if v["cluster_y"] == 1:
+            assert v["ly"] > 2 * R * v["tb"]
+        else:
+            # cluster CTAs: the outer ones keep (tb - 1) R halo rows on their outer side
+            assert v["tb"] >= 2 and v["ly"] - R - R * v["tb"] > 0 and v["cluster_y"] <= 16
     # every kind has a single-step variant and R=1 kinds fuse at least 4 steps
     for k in range(4):
         assert any(v["kind"] == k and v["tb"] == 1 for v in vs)

@@ -98,6 +98,49 @@ def test_every_variant(girih, oracle, kind):
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_cluster_variants(girih, oracle, kind):
+    # thread-block clusters along y (the fused levels' halo rows shared through distributed
+    # shared memory): several clusters per tile column with a partial last one, odd extents,
+    # pad, forced z chunks, and a continuation from an odd start level
+    g = girih
+    cl = [v for v in g.variants() if v["kind"] == kind and v["cluster_y"] > 1]
+    if not cl:
+        pytest.skip("no cluster variant compiled for this kind")
+    dims = (45, 157, 21, 1) if kind < 2 else (47, 131, 23, 1)
+    base = oracle.init_state(kind, *dims, 17, remap=True)
+    for v in cl:
+        tb = v["tb"]
+        for steps, zc in ((2 * tb + 1, 0), (3 * tb, 3)):
+            ref = base.copy()
+            oracle.naive_sweep(ref, steps)
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb, variant=v["index"], zchunks=zc))
+            assert_state_equal(st, ref, f"cluster variant {v} T={steps} zc={zc}")
+        ref = base.copy()
+        oracle.naive_sweep(ref, 2 * tb + 3)
+        st = to_problem(g, base)
+        g.run(st, 3, g.GpuConfig(tb=1))
+        g.run(st, 2 * tb, g.GpuConfig(tb=tb, variant=v["index"]))
+        assert_state_equal(st, ref, f"cluster variant {v} odd start")
+
+
+@pytest.mark.parametrize("slabs", [0, 3])
+def test_row_digest_matches_oracle(girih, oracle, slabs):
+    # girih_gpu_row_digest (device, one thread per row) == orc_row_digest (host), every field
+    g = girih
+    base = oracle.init_state(3, 21, 18, 25, 3, 6, remap=True)
+    ref = base.copy()
+    oracle.naive_sweep(ref, 3)
+    with g.DeviceState.seeded(3, g.GridSpec(21, 18, 25, 3), 6, remap=True,
+                              config=g.GpuConfig(emulate_slabs=slabs)) as ds:
+        ds.step(3)
+        assert ds.row_digest("u") == oracle.row_digest(ref.u)
+        assert ds.row_digest("v") == oracle.row_digest(ref.v)
+        for c in (0, 12):
+            assert ds.row_digest(c) == oracle.row_digest(ref.coeffs[c])
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_minimum_grid(girih, oracle, kind):
     # smallest admissible extents 2R+1 (stencil.cpp:61-63)
     g = girih
@@ -515,14 +558,17 @@ def test_bench_multirank_path_functional(girih):
     env = dict(os.environ, GIRIH_BENCH_SHARED_GPU="1", MASTER_ADDR="127.0.0.1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29631", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--no-e2e"]
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--n", "256", "--nt", "20"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout[-3000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and "NOT a measurement" in d["data"]
-    assert "pushed by each pass" in d["config"]["parallelism"]
+    assert d["scaling"] == "strong" and d["gpu"]["global_grid"] == [256, 256, 256]
+    assert "pushed by each pass" in d["gpu"]["parallelism"]
+    # rank 0's drop-in call on pageable host buffers
+    assert d["e2e"]["value"] > 0 and "pageable" in d["e2e"]["host_memory"]
 
 
 def test_handles_on_concurrent_host_threads(girih, oracle):

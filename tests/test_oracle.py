@@ -180,3 +180,18 @@ def test_config1_checksum_matches_survey(oracle):
     s = oracle.init_state(0, 256, 256, 256, 0, 42, remap=True)
     oracle.naive_sweep(s, 100)
     assert oracle.interior_checksum(s) == 0x9F26250C918339D4
+
+
+def test_row_digest_definition(oracle):
+    # FNV-1a over the per-row FNV-1a hashes (the C5 fixtures' digest), restated in Python
+    import numpy as np
+    a = np.random.default_rng(3).random((3, 4, 5))
+
+    def fnv(bs, h=0xCBF29CE484222325):
+        for b in bs:
+            h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+        return h
+
+    rows = [fnv(a[k, j].tobytes()) for k in range(3) for j in range(4)]
+    want = fnv(b"".join(r.to_bytes(8, "little") for r in rows))
+    assert oracle.row_digest(a) == want

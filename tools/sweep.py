@@ -19,14 +19,18 @@ ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--nt", type=int, default=24)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--variants", default="all")
-ap.add_argument("--zchunks", type=int, default=0)
+ap.add_argument("--zchunks", default="0", help="comma list of z-chunk counts (0 = model)")
+ap.add_argument("--tbs", default="", help="comma list of fused depths to sweep (default all)")
+ap.add_argument("--clusters", default="all", choices=["all", "only", "none"])
 a = ap.parse_args()
 for kind in [int(k) for k in a.kinds.split(",")]:
-    vs = [v for v in g.variants() if v["kind"] == kind]
+    vs = [v for v in g.variants() if v["kind"] == kind and
+          (not a.tbs or v["tb"] in [int(t) for t in a.tbs.split(",")]) and
+          (a.clusters == "all" or (v["cluster_y"] > 1) == (a.clusters == "only"))]
     grid = g.GridSpec(a.n, a.n, a.n, 0)
     with g.DeviceState.seeded(kind, grid, 42, remap=True) as ds:
-        for v in vs:
-            ds.set_config(g.GpuConfig(tb=v["tb"], variant=v["index"], zchunks=a.zchunks))
+        for v, zc in [(v, int(z)) for v in vs for z in a.zchunks.split(",")]:
+            ds.set_config(g.GpuConfig(tb=v["tb"], variant=v["index"], zchunks=zc))
             ds.step(a.nt)
             best = None
             for _ in range(a.reps):
@@ -35,7 +39,8 @@ for kind in [int(k) for k in a.kinds.split(",")]:
                     best = r
             avg = best.pass_seconds / best.n_launches
             print(json.dumps({"kind": g.KINDS[kind], "n": a.n, "tb": v["tb"], "variant": v["index"],
-                              "lx": v["lx"], "ly": v["ly"], "mlups": round(best.mlups),
+                              "lx": v["lx"], "ly": v["ly"], "threads": v["threads"],
+                              "cy": v["cluster_y"], "mlups": round(best.mlups),
                               "avg_pass_ms": round(avg * 1e3, 4), "passes": best.n_launches,
                               "eff_GBs": round(a.n ** 3 * B1[kind] / avg / 1e9, 1),
                               "zchunks": best.zchunks_used, "grid": best.grid_ctas,
