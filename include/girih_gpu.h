@@ -92,6 +92,8 @@ typedef struct {
     int streamed;           /* girih_gpu_run: 1 = uploads, passes and downloads pipelined along z
                                (skewed task graph; kernel_s is then the whole device span) */
     int n_passes;           /* stencil passes (a chained launch runs several) */
+    long long units;        /* work units executed (tile column x z chunk per pass): the GPU
+                               counterpart of PerfReport::tiles (engine.hpp:93-98) */
 } girih_gpu_report;
 
 /* kernel variant description (compiled tile shapes) */
@@ -163,6 +165,36 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
                       long long* first_index);
 
 /* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
+/* Instrumented drop-in call: the counterpart of the reference's RunOptions
+ * (proj/include/girih/engine.hpp:100-103, engine.cpp:358-364, 413-416). One device, one launch
+ * per pass. `trace_cb` receives one record per work unit (the GPU counterpart of the reference's
+ * diamond tile: a tile column x z chunk of one pass) with the CTA that ran it and its
+ * %globaltimer start/end, sorted by (pass, unit); `ledger` (steps * nx * ny * nz counts,
+ * [t][z][y][x] in interior coordinates, t relative to the call's first step) receives how many
+ * times each cell update was produced by the unit that owns it -- exactly once when the tiling,
+ * z chunks and slabs partition the grid (UpdateLedger::all_exactly_once, engine.hpp:74-91). */
+typedef struct {
+    int pass;        /* pass index within the call */
+    int unit;        /* work unit within the pass */
+    int cta;         /* CTA (block index) that ran it: the reference's thread group */
+    int sm;          /* SM it ran on */
+    unsigned long long start_ns, end_ns;
+} girih_gpu_trace_record;
+
+typedef void (*girih_gpu_trace_fn)(void* ctx, const girih_gpu_trace_record* recs, long long n);
+
+typedef struct {
+    girih_gpu_trace_fn trace_cb;  /* NULL: no trace */
+    void* trace_ctx;
+    long long trace_capacity;     /* records kept (0: 1M); trace_total reports all units */
+    long long trace_total;        /* out */
+    unsigned int* ledger;         /* NULL: no ledger; else steps * nx * ny * nz counts (out) */
+} girih_gpu_run_options;
+
+/* girih_gpu_run with instrumentation (opts NULL or empty: exactly girih_gpu_run) */
+int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
+                     girih_gpu_report* report, girih_gpu_run_options* opts);
+
 /* Device-side digest of a whole field (0 = u, 1 = v, 2 + c = coefficient c), ghosts and pad
  * included: FNV-1a over the FNV-1a hashes of every allocated row in (k, j) order (one GPU
  * thread per row). A checksum of checksums of the full state that needs no download; the

@@ -11,6 +11,8 @@
 // std::runtime_error for CUDA / NCCL / out-of-memory failures.
 #pragma once
 
+#include <algorithm>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -94,7 +96,7 @@ inline GpuReport run(ProblemState& state, long steps, const GpuConfig& cfg) {
     out.wall_seconds = r.wall_s;
     out.lups = r.lups;
     out.glups = r.wall_s > 0 ? r.lups / r.wall_s / 1e9 : 0.0;
-    out.tiles = r.n_launches;
+    out.tiles = r.units;  // work units (tile column x z chunk per pass)
     out.kernel_seconds = r.kernel_s;
     out.h2d_seconds = r.h2d_s;
     out.d2h_seconds = r.d2h_s;
@@ -105,14 +107,27 @@ inline GpuReport run(ProblemState& state, long steps, const GpuConfig& cfg) {
     return out;
 }
 
+namespace detail {
+inline void write_trace_csv(void* ctx, const girih_gpu_trace_record* r, long long n) {
+    // the reference's TileScheduler::dump_trace_csv columns (scheduler.cpp:96-101): a GPU
+    // "tile" is a work unit (pass, tile column x z chunk), its "group" the CTA that ran it
+    std::ostream& os = *static_cast<std::ostream*>(ctx);
+    os << "tile,group,start_ns,end_ns\n";
+    for (long long i = 0; i < n; ++i)
+        os << i << ',' << r[i].cta << ',' << r[i].start_ns << ',' << r[i].end_ns << '\n';
+}
+}  // namespace detail
+
 // Signature-compatible drop-in for girih::run (engine.hpp:113-115). The CPU-engine parameters
 // are validated exactly as the reference validates them (so inadmissible configurations still
-// throw std::invalid_argument) and are otherwise not used by the GPU path.
+// throw std::invalid_argument; engine.cpp:270-290, 333-337, geometry.cpp:9-15, 39-43) and are
+// otherwise not used by the GPU path. RunOptions (engine.hpp:100-103) are honoured: trace_out
+// receives the per-unit execution trace CSV and ledger the exactly-once update counts of the
+// GPU run (girih_gpu_run_ex).
 inline PerfReport run(ProblemState& state, long steps, int dw, const WavefrontSpec& wf,
                       const ThreadGroupShape& shape, WavefrontVariant variant, int n_groups,
                       const RunOptions& opts = {}, const GpuConfig& cfg = {}) {
     (void)variant;
-    (void)opts;
     // engine.cpp:285-290, 333-335
     if (shape.tx < 1 || shape.ty < 1 || shape.tz < 1)
         throw std::invalid_argument("thread group axes must be positive");
@@ -128,8 +143,52 @@ inline PerfReport run(ProblemState& state, long steps, int dw, const WavefrontSp
         if (state.grid.ny < dw || state.grid.ny % dw != 0)
             throw std::invalid_argument("build_tessellation: Ny must be a multiple of D_w");
         if (wf.nf < 1) throw std::invalid_argument("wavefront_width: need R >= 1, N_F >= 1, D_w >= 2R");
+        // resolve_block_size (engine.cpp:270-283): the wavefront block must split over T_z
+        const int ww = wavefront_width(dw, wf.nf, R);
+        int bs = wf.bs_z > 0 ? wf.bs_z : default_block_size(ww, shape.tz);
+        if (wf.bs_z <= 0) {
+            const int unit = default_block_size(1, shape.tz);
+            const int cap = std::max(unit, (state.grid.nz + unit - 1) / unit * unit);
+            bs = std::min(bs, cap);
+        }
+        if (bs < shape.tz || bs % shape.tz != 0)
+            throw std::invalid_argument("wavefront block size must be a positive multiple of T_z");
     }
-    return run(state, steps, cfg);
+    if (!opts.trace_out && !opts.ledger) return run(state, steps, cfg);
+    // instrumented run
+    StateView sv(state);
+    girih_gpu_config c = to_c(cfg);
+    girih_gpu_report r{};
+    girih_gpu_run_options o{};
+    if (opts.trace_out) {
+        o.trace_cb = &detail::write_trace_csv;
+        o.trace_ctx = opts.trace_out;
+    }
+    std::vector<unsigned> counts;
+    if (opts.ledger) {
+        counts.assign(static_cast<size_t>(steps) * state.grid.nx * state.grid.ny * state.grid.nz, 0u);
+        o.ledger = counts.data();
+    }
+    check(girih_gpu_run_ex(&sv.v, steps, &c, &r, &o));
+    state.t_current = static_cast<long>(sv.v.t_current);
+    if (opts.ledger) {
+        const size_t cells = static_cast<size_t>(state.grid.nx) * state.grid.ny * state.grid.nz;
+        for (long t = 0; t < steps; ++t)
+            for (int z = 0; z < state.grid.nz; ++z)
+                for (int y = 0; y < state.grid.ny; ++y)
+                    for (int x = 0; x < state.grid.nx; ++x) {
+                        const unsigned n = counts[t * cells +
+                                                  (static_cast<size_t>(z) * state.grid.ny + y) *
+                                                      state.grid.nx + x];
+                        for (unsigned k = 0; k < n; ++k) opts.ledger->record(t, z, y, x, 0);
+                    }
+    }
+    PerfReport out;
+    out.wall_seconds = r.wall_s;
+    out.lups = r.lups;
+    out.glups = r.wall_s > 0 ? r.lups / r.wall_s / 1e9 : 0.0;
+    out.tiles = o.trace_total;
+    return out;
 }
 
 }  // namespace gpu

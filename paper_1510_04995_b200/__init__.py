@@ -7,7 +7,7 @@ from ._lib import GirihError, InvalidArgument, LIB_PATH, load
 from .stencil import (CONST7PT, CONST25PT, KINDS, VAR7PT, VAR25PT, DeviceState, GpuConfig,
                       GridSpec, PerfReport, ProblemState, StencilTraits, device_info, fp64_peak,
                       init_state, interior_checksum, model, nccl_unique_id, pinned_empty, plan,
-                      run, trim,
+                      run, run_instrumented, trim,
                       slab_layout,
                       stencil_from_name,
                       traits, variants)
@@ -16,5 +16,5 @@ __all__ = [
     "CONST7PT", "VAR7PT", "CONST25PT", "VAR25PT", "KINDS", "DeviceState", "GpuConfig", "GridSpec",
     "PerfReport", "ProblemState", "StencilTraits", "GirihError", "InvalidArgument", "LIB_PATH",
     "device_info", "fp64_peak", "init_state", "interior_checksum", "load", "model", "nccl_unique_id", "pinned_empty", "plan",
-    "run", "slab_layout", "stencil_from_name", "traits", "trim", "variants",
+    "run", "run_instrumented", "slab_layout", "stencil_from_name", "traits", "trim", "variants",
 ]

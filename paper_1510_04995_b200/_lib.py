@@ -53,7 +53,7 @@ class GirihGpuReport(C.Structure):
         ("pass_s", C.c_double), ("computed_lups", C.c_longlong),
         ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong),
         ("variant_used", C.c_int), ("zchunks_used", C.c_int), ("grid_ctas", C.c_int),
-        ("streamed", C.c_int), ("n_passes", C.c_int),
+        ("streamed", C.c_int), ("n_passes", C.c_int), ("units", C.c_longlong),
     ]
 
 
@@ -61,6 +61,20 @@ class GirihGpuVariant(C.Structure):
     _fields_ = [("kind", C.c_int), ("tb", C.c_int), ("lx", C.c_int), ("ly", C.c_int),
                 ("threads", C.c_int), ("prefetch", C.c_int), ("smem_bytes", C.c_int),
                 ("cluster_y", C.c_int), ("aux_prefetch", C.c_int)]
+
+
+class GirihGpuTraceRecord(C.Structure):
+    _fields_ = [("pass_", C.c_int), ("unit", C.c_int), ("cta", C.c_int), ("sm", C.c_int),
+                ("start_ns", C.c_ulonglong), ("end_ns", C.c_ulonglong)]
+
+
+GIRIH_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(GirihGpuTraceRecord), C.c_longlong)
+
+
+class GirihGpuRunOptions(C.Structure):
+    _fields_ = [("trace_cb", GIRIH_TRACE_FN), ("trace_ctx", C.c_void_p),
+                ("trace_capacity", C.c_longlong), ("trace_total", C.c_longlong),
+                ("ledger", C.POINTER(C.c_uint))]
 
 
 # every symbol include/girih_gpu.h declares, with (restype, argtypes)
@@ -97,6 +111,7 @@ SIGNATURES = {
     "girih_gpu_download": (C.c_int, [C.c_void_p, C.POINTER(GirihStateView)]),
     "girih_gpu_download_coeffs": (C.c_int, [C.c_void_p, C.POINTER(_dp), C.c_int, _dp]),
     "girih_gpu_row_digest": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]),
+    "girih_gpu_run_ex": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
     "girih_gpu_get_t": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "girih_gpu_set_config": (C.c_int, [C.c_void_p, C.POINTER(GirihGpuConfig)]),
     "girih_gpu_close": (C.c_int, [C.c_void_p]),

@@ -484,7 +484,7 @@ struct DevBuf {
 struct StepStats {
     int n_launches = 0, n_passes = 0;
     double pass_s = 0;
-    long long computed = 0;
+    long long computed = 0, units = 0;
     int grid = 0, zchunks = 0, variant = -1, tb_used = 0;
 };
 
@@ -556,6 +556,14 @@ struct Handle {
         StepStats st;
     };
     std::vector<GraphEntry> graphs;
+    // instrumentation of girih_gpu_run_ex (single device, one launch per pass): per-unit trace
+    // records and the owned-update ledger (zwave.cuh PassParams::trace / ::ledger)
+    struct Instr {
+        bool on = false;
+        std::unique_ptr<DevBuf> trace, ledger;  // trace: cap * 4 records + 1 counter
+        long long cap = 0, t_begin = 0;
+        int npass = 0;
+    } instr;
 
     size_t plane_elems() const { return size_t(pitch) * Y; }
     size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
@@ -1164,11 +1172,11 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.zc_len = tg.zc_len;
     p.units = tg.units;
     p.work = reinterpret_cast<int*>(s.work->p);
-    p.trace = nullptr;
+    p.ptrace = nullptr;
     if (std::getenv("GIRIH_TRACE")) {
         alloc_buf(s.trace, s.device, 4096 * 8, s.stream);
         GCHECK(cudaMemsetAsync(s.trace->p, 0, 4096 * 8 * 8, s.stream));
-        p.trace = reinterpret_cast<unsigned long long*>(s.trace->p);
+        p.ptrace = reinterpret_cast<unsigned long long*>(s.trace->p);
     }
     if (h.ipc && zlo == s.zout_lo && zhi == s.zout_hi) {
         const long long plane = (long long)h.pitch * h.Y;
@@ -1200,6 +1208,17 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
         p.push_hz = h.hz;
     }
     // cluster variants: cy CTAs per unit, the grid a whole number of clusters
+    if (h.instr.on) {
+        if (h.instr.trace) {
+            p.trace = reinterpret_cast<unsigned long long*>(h.instr.trace->p);
+            p.trace_n = p.trace + 4 * h.instr.cap;
+            p.trace_cap = h.instr.cap;
+        }
+        if (h.instr.ledger) {
+            p.ledger = reinterpret_cast<unsigned*>(h.instr.ledger->p);
+            p.ledger_t = int(t0 - h.instr.t_begin);
+        }
+    }
     li->grid = std::min(p.units * var->cy, max_grid / var->cy * var->cy);
     li->zchunks = p.nzc;
     li->computed_lups = tg.computed_lups;
@@ -1528,6 +1547,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 GCHECK(cvar->launch_chain(cmap, cd, p, li.grid, s.stream));
                 if (time_passes) GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
                 st.computed += li.computed_lups * npass;
+                st.units += (long long)p.units * npass;
                 st.grid = li.grid;
                 st.zchunks = li.zchunks;
                 st.variant = global_index_of(cvar);
@@ -1565,12 +1585,13 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             if (time_passes && g == 0)
                 GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi], s.stream, evflag));
             const PassDesc pd = single_desc(h, int(g), var, ps.tb, p, vmap, *umap);
-            GCHECK(var->launch(*cmap, pd, p, li.grid, s.stream));
+            if (h.instr.on) p.trace_pass = h.instr.npass;
+            GCHECK((h.instr.on ? var->launch_instr : var->launch)(*cmap, pd, p, li.grid, s.stream));
             if (time_passes && g == 0)
                 GCHECK(cudaEventRecordWithFlags(h.ev[2 * pi + 1], s.stream, evflag));
-            if (p.trace) {  // debug: dump CTA 0's phase clocks of this pass
+            if (p.ptrace) {  // debug: dump CTA 0's phase clocks of this pass
                 std::vector<unsigned long long> tv(4096 * 8);
-                GCHECK(cudaMemcpyAsync(tv.data(), p.trace, tv.size() * 8, cudaMemcpyDeviceToHost,
+                GCHECK(cudaMemcpyAsync(tv.data(), p.ptrace, tv.size() * 8, cudaMemcpyDeviceToHost,
                                        s.stream));
                 GCHECK(cudaStreamSynchronize(s.stream));
                 if (FILE* f = std::fopen(std::getenv("GIRIH_TRACE"), "a")) {
@@ -1582,10 +1603,12 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 }
             }
             st.computed += li.computed_lups;
+            st.units += p.units;
             st.grid = li.grid;
             st.zchunks = li.zchunks;
             st.n_launches++;
         }
+        if (h.instr.on) ++h.instr.npass;
         // halo exchange of the levels the next pass reads: pushed by the pass itself
         // (single-process slabs; the next pass only waits for its neighbours), or copied
         if (h.ipc) {
@@ -1971,7 +1994,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     const Variant* var2 =
         single ? nullptr : select_variant(h.kind, 2, h.cfg.tb == 2 ? h.cfg.variant : -1);
     const Variant* var1 = select_variant(h.kind, 1, h.cfg.tb == 1 ? h.cfg.variant : -1);
-    long long computed = 0;
+    long long computed = 0, units = 0;
     int launches = 0;
     // final level of parity b (single-step mode: the parity-b field itself)
     double* fin_b = single ? rot[0] : tail1 ? rot[(npass - 1) % 3] : rot[npass % 3];
@@ -2088,6 +2111,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
                 const PassDesc pd = single_desc(h, 0, var, tb, p, vmap, umap);
                 GCHECK(var->launch(cmap, pd, p, li.grid, st));
                 computed += li.computed_lups;
+                units += p.units;
                 ++launches;
             }
             GCHECK(cudaEventRecord(ev_task[size_t(c) * npass + q], st));
@@ -2133,6 +2157,7 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
         rep->n_launches = launches;
         rep->n_passes = launches;
         rep->computed_lups = computed;
+        rep->units = units;
         rep->h2d_bytes = (long long)(cells * 8 * (shell ? 1 + h.nc : 2 + h.nc)) +
                          (shell ? shell_off(h.Z) * 8 : 0);
         rep->d2h_bytes = (long long)(size_t(h.X) * h.Y * h.nz * 8 * 2);
@@ -2191,6 +2216,7 @@ double step_timed(Handle& h, long long steps, girih_gpu_report* rep) {
         rep->n_passes = st.n_passes;
         rep->pass_s = st.pass_s;
         rep->computed_lups = st.computed;
+        rep->units = st.units;
         rep->variant_used = st.variant;
         rep->zchunks_used = st.zchunks;
         rep->grid_ctas = st.grid;
@@ -2631,6 +2657,96 @@ int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_conf
             report->d2h_bytes = (long long)(cells * 8 * 2);
             report->wall_s = std::chrono::duration<double>(b1 - w0).count();
             report->mlups = report->wall_s > 0 ? report->lups / report->wall_s / 1e6 : 0.0;
+        }
+        destroy(h);
+        h = nullptr;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
+                     girih_gpu_report* report, girih_gpu_run_options* opts) {
+    if (!opts || (!opts->ledger && !opts->trace_cb)) return girih_gpu_run(state, steps, cfg, report);
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!state) throw_err(GIRIH_EINVAL, "null argument");
+        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
+        {
+            Handle probe;
+            setup_geometry(probe, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        }
+        opts->trace_total = 0;
+        if (steps == 0) {
+            if (report) std::memset(report, 0, sizeof *report);
+            return;
+        }
+        girih_gpu_config c = cfg ? *cfg : default_config();
+        if (c.ngpus > 1)
+            throw_err(GIRIH_EINVAL, "instrumented runs use one device (emulated slabs allowed)");
+        c.chain = -1;   // one launch per pass: every unit belongs to one pass
+        c.graphs = -1;
+        const auto w0 = std::chrono::steady_clock::now();
+        h = new Handle();
+        h->uploads_all = true;
+        h->cfg = c;
+        setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        upload_state(*h, *state);
+        Slab& s0 = h->slabs[0];
+        const size_t cells = size_t(h->nx) * h->ny * h->nz;
+        h->instr.on = true;
+        h->instr.t_begin = state->t_current;
+        if (opts->ledger) {
+            alloc_buf(h->instr.ledger, s0.device, (size_t(steps) * cells + 1) / 2, s0.stream);
+        }
+        if (opts->trace_cb) {
+            h->instr.cap = opts->trace_capacity > 0 ? opts->trace_capacity : (1ll << 20);
+            alloc_buf(h->instr.trace, s0.device, size_t(h->instr.cap) * 4 + 1, s0.stream);
+        }
+        girih_gpu_report r{};
+        step_timed(*h, steps, &r);
+        std::vector<double*> d(h->slabs.size());
+        for (int f = 0; f < 2; ++f) {
+            for (size_t g = 0; g < h->slabs.size(); ++g) d[g] = h->slabs[g].buf[f]->p;
+            copy_d2h(*h, d.data(), f == 0 ? state->u : state->v);
+        }
+        GCHECK(cudaSetDevice(s0.device));
+        if (opts->ledger)
+            GCHECK(cudaMemcpyAsync(opts->ledger, h->instr.ledger->p, size_t(steps) * cells * 4,
+                                   cudaMemcpyDeviceToHost, s0.stream));
+        std::vector<unsigned long long> raw;
+        unsigned long long n = 0;
+        if (opts->trace_cb) {
+            const auto* tp = reinterpret_cast<const unsigned long long*>(h->instr.trace->p);
+            GCHECK(cudaMemcpyAsync(&n, tp + 4 * h->instr.cap, 8, cudaMemcpyDeviceToHost, s0.stream));
+            GCHECK(cudaStreamSynchronize(s0.stream));
+            raw.resize(size_t(std::min<long long>((long long)n, h->instr.cap)) * 4);
+            GCHECK(cudaMemcpyAsync(raw.data(), tp, raw.size() * 8, cudaMemcpyDeviceToHost, s0.stream));
+        }
+        sync_all(*h);
+        state->t_current = h->t_current;
+        if (opts->trace_cb) {
+            std::vector<girih_gpu_trace_record> recs(raw.size() / 4);
+            for (size_t q = 0; q < recs.size(); ++q) {
+                recs[q].pass = int(raw[4 * q] >> 32);
+                recs[q].unit = int(raw[4 * q] & 0xffffffffu);
+                recs[q].cta = int(raw[4 * q + 1] >> 32);
+                recs[q].sm = int(raw[4 * q + 1] & 0xffffffffu);
+                recs[q].start_ns = raw[4 * q + 2];
+                recs[q].end_ns = raw[4 * q + 3];
+            }
+            std::sort(recs.begin(), recs.end(), [](const auto& a, const auto& b) {
+                return a.pass != b.pass ? a.pass < b.pass : a.unit < b.unit;
+            });
+            opts->trace_total = (long long)n;
+            opts->trace_cb(opts->trace_ctx, recs.data(), (long long)recs.size());
+        }
+        if (report) {
+            *report = r;
+            report->wall_s =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
         }
         destroy(h);
         h = nullptr;

@@ -20,6 +20,7 @@ struct Variant {
     int smem_bytes;
     int aux_x0, aux_y0, aux_x, aux_y;  // coefficient (aux) box inside the tile
     LaunchFn launch;             // one pass
+    LaunchFn launch_instr;       // one pass with the trace / ledger instrumentation compiled in
     LaunchChainFn launch_chain;  // cd.npass chained passes over the same tile grid (cy == 1)
     OccFn occupancy;             // resident CTAs, single-pass kernel (a multiple of cy)
     OccFn occupancy_chain;       // the same for the chained kernel
@@ -35,11 +36,12 @@ extern const int kNumVariantsConst25;
 extern const Variant kVariantsVar25[];
 extern const int kNumVariantsVar25;
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY,
+          bool INSTR = false>
 cudaError_t launch_zwave_impl(const CUtensorMap& cmap, const ChainDescs& cd, const PassParams& p,
                               int grid, cudaStream_t stream) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY>;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY, INSTR>;
     // once per instantiation (thread-safe static initialisation)
     static const cudaError_t attr =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
@@ -81,7 +83,7 @@ cudaError_t launch_zwave_chain(const CUtensorMap& cmap, const ChainDescs& cd, co
 }
 
 // one pass = a chain of length 1 (no dependency flags)
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY, bool INSTR = false>
 cudaError_t launch_zwave(const CUtensorMap& cmap, const PassDesc& d, const PassParams& p, int grid,
                          cudaStream_t stream) {
     ChainDescs cd{};
@@ -89,7 +91,8 @@ cudaError_t launch_zwave(const CUtensorMap& cmap, const PassDesc& d, const PassP
     cd.pidx[0] = 0;
     cd.npass = 1;
     cd.done = nullptr;
-    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false, CY>(cmap, cd, p, grid, stream);
+    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false, CY, INSTR>(cmap, cd, p, grid,
+                                                                                   stream);
 }
 
 template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY, bool CHAIN = false>
@@ -145,6 +148,7 @@ cudaError_t occupancy_zwave(int* max_ctas) {
             ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AX,                           \
             ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AY,                           \
             &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                             \
+            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY, true>,                       \
             &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                       \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                          \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY, true>                     \

@@ -94,7 +94,7 @@ struct PassParams {
     int oz0;                 // local plane of the output store map's z = 0 (the slab's zout_lo)
     int units;               // tiles_x * tiles_y * nzc
     int* work;               // dynamic unit counter (zeroed before every launch)
-    unsigned long long* trace;  // optional per-iteration phase clocks of CTA 0 (debug)
+    unsigned long long* ptrace;  // optional per-iteration phase clocks of CTA 0 (debug)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
                              // innermost box coordinate 16-byte aligned (even for fp64)
     // Halo push (single-process z-slabs): the output cells of this slab's bottom / top push_hz
@@ -107,6 +107,16 @@ struct PassParams {
     double* push_up_penult;
     long long push_dn_off, push_up_off;
     int push_hz;
+    // Instrumentation (girih_gpu_run_ex, the reference's RunOptions, engine.hpp:100-103; off
+    // when null): per-unit trace records appended at trace[4 * atomicAdd(trace_n, 1)] =
+    // {pass << 32 | unit, cta << 32 | sm, start ns, end ns} (%globaltimer), and the ledger of
+    // owned cell updates [step][z][y][x] (interior coordinates), +1 per output cell and level.
+    unsigned long long* trace;
+    unsigned long long* trace_n;
+    long long trace_cap;
+    int trace_pass;
+    unsigned* ledger;
+    int ledger_t;  // step index (from the start of the call) of this pass's level 1
 };
 
 // Pass chaining. One launch may run a sequence of passes over the same tile grid. Units are
@@ -241,6 +251,17 @@ __device__ __forceinline__ void st_cluster_d2(uint32_t addr, double2 v) {
 }
 __device__ __forceinline__ void st_cluster_s32(uint32_t addr, int v) {
     asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned sm_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
 }
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -454,13 +475,15 @@ struct ZwaveConfig {
 // CHAIN = false: one pass (descriptors d[0]); true: cd.npass chained passes. The two are
 // separate instantiations so that single-pass launches carry none of the chaining state (the
 // 128-register var7pt CTA spills otherwise, and shared-memory producer state cost 30%).
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY = 1>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY = 1,
+          bool INSTR = false>
 __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 1) ? MINB - 1 : MINB)
     zwave_kernel(const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
                  const __grid_constant__ ChainDescs cd,     // per-pass buffers and maps
                  const __grid_constant__ PassParams p) {
     using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
     static_assert(CY == 1 || !CHAIN, "cluster kernels run single passes");
+    static_assert(!INSTR || !CHAIN, "instrumented kernels run single passes");
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
     constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA;
     constexpr int OWN = CFG::OWN, OYC = CFG::OYC;
@@ -716,6 +739,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 
     __syncthreads();  // uq[0] visible
     uint32_t g = G0;  // consumer's global element index
+    unsigned long long unit_t0 = 0;  // instrumentation: start of thread 0's current unit
     for (int seq = 0;; ++seq) {
         const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
         if (u >= total) break;
@@ -767,11 +791,11 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             const int j = ug.za - H + it;  // level-0 plane of this iteration
             __syncthreads();               // previous iteration's smem reads/writes are complete
 #ifdef GIRIH_ZWAVE_TRACE
-            const bool tr = p.trace && blockIdx.x == 0 && (tid == 0 || tid == 32) && g - G0 < 4096;
+            const bool tr = p.ptrace && blockIdx.x == 0 && (tid == 0 || tid == 32) && g - G0 < 4096;
 #else
             constexpr bool tr = false;  // build with -DGIRIH_ZWAVE_TRACE for phase clocks
 #endif
-            unsigned long long* trp = tr ? p.trace + ((g - G0) * 2 + (tid == 32)) * 4 : nullptr;
+            unsigned long long* trp = tr ? p.ptrace + ((g - G0) * 2 + (tid == 32)) * 4 : nullptr;
             if (tr) trp[0] = clock64();
             if (tid == STORE_TID) {
                 stored_now = false;
@@ -1084,6 +1108,22 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                                 pen[colidx[b + 1]] = c2.y;
                         }
                     }
+                    if (INSTR && p.ledger) {  // instrumentation: this unit owns these updates
+                        const int kz = k + p.zoff - R;
+                        if (kz >= 0 && kz < p.nzg) {
+#pragma unroll
+                            for (int i = 0; i < PPT; ++i)
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) {
+                                    const int b = 2 * i + q;
+                                    if (!((out_mask >> b) & 1) || ((ghost_mask >> b) & 1)) continue;
+                                    const int xa = xa0 + (lcell[i] + q) % LX, ya = ya0 + lcell[i] / LX;
+                                    const long long cell = ((long long)kz * p.ny + (ya - R)) * p.nx + (xa - R);
+                                    for (int s2 = 0; s2 < TB; ++s2)
+                                        atomicAdd(p.ledger + (long long)(p.ledger_t + s2) * p.nzg * p.ny * p.nx + cell, 1u);
+                                }
+                        }
+                    }
                     if constexpr (!CHAIN) {
                         // halo push: boundary planes go to the neighbour slab as they are made
                         const bool dn = p.push_dn_final && k < p.zout_lo + p.push_hz;
@@ -1184,6 +1224,19 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             }
             if constexpr (CHAIN)
                 if (tid == STORE_TID && it == n_it - 1) pub_next = u;  // unit finished
+            if (INSTR && p.trace && tid == 0) {  // instrumentation: one record per unit
+                if (it == 0) unit_t0 = global_ns();
+                if (it == n_it - 1) {
+                    const unsigned long long r = atomicAdd(p.trace_n, 1ull);
+                    if ((long long)r < p.trace_cap) {
+                        unsigned long long* rec = p.trace + 4 * r;
+                        rec[0] = ((unsigned long long)p.trace_pass << 32) | unsigned(u);
+                        rec[1] = ((unsigned long long)blockIdx.x << 32) | sm_id();
+                        rec[2] = unit_t0;
+                        rec[3] = global_ns();
+                    }
+                }
+            }
             // three staging planes: the plane the next iteration writes was handed to the store
             // issued two iterations ago, so only that older store must have finished reading
             if (tid == STORE_TID) {

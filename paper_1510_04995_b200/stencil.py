@@ -25,7 +25,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (GirihGpuConfig, GirihGpuReport, GirihGpuVariant, GirihStateView, InvalidArgument,
+from ._lib import (GIRIH_TRACE_FN, GirihGpuConfig, GirihGpuReport, GirihGpuRunOptions, GirihGpuVariant, GirihStateView, InvalidArgument,
                    check, load)
 
 KINDS = ("const7pt", "var7pt", "const25pt", "var25pt")
@@ -136,13 +136,14 @@ class PerfReport:
     grid_ctas: int = 0
     streamed: int = 0  # girih_gpu_run pipelined the copies with the passes along z
     n_passes: int = 0  # stencil passes (a chained launch runs several)
+    units: int = 0     # work units (tile column x z chunk per pass): PerfReport::tiles
 
     @staticmethod
     def from_c(r: GirihGpuReport) -> "PerfReport":
         return PerfReport(r.wall_s, r.kernel_s, r.lups, r.mlups / 1e3, r.mlups, r.h2d_s, r.d2h_s,
                           r.model_bytes_per_lup, r.tb_used, r.n_launches, r.pass_s,
                           r.computed_lups, r.h2d_bytes, r.d2h_bytes, r.variant_used,
-                          r.zchunks_used, r.grid_ctas, r.streamed, r.n_passes)
+                          r.zchunks_used, r.grid_ctas, r.streamed, r.n_passes, r.units)
 
 
 def variants():
@@ -217,6 +218,40 @@ def plan(kind: int, t0: int, steps: int, tb: int):
     arrs = [(C.c_int * cap)() for _ in range(5)]
     check(lib.girih_gpu_plan(int(kind), int(t0), int(steps), int(tb), cap, C.byref(n), *arrs))
     return [tuple(a[i] for a in arrs) for i in range(n.value)]
+
+
+def run_instrumented(state: ProblemState, steps: int, config: Optional[GpuConfig] = None,
+                     trace: bool = True, ledger: bool = True):
+    """girih_gpu_run_ex: the drop-in call with the reference's RunOptions instrumentation
+    (engine.hpp:100-103). Returns (report, trace, ledger): `trace` a structured array of
+    per-unit records (pass, unit, cta, sm, start_ns, end_ns), sorted by (pass, unit); `ledger`
+    the [steps][nz][ny][nx] counts of owned cell updates (all 1 when the run covered every cell
+    update exactly once)."""
+    config = config or GpuConfig()
+    cfg = config.to_c()
+    rep = GirihGpuReport()
+    v = _View(state)
+    opts = GirihGpuRunOptions()
+    recs = []
+
+    def collect(_ctx, ptr, n):
+        for i in range(n):
+            r = ptr[i]
+            recs.append((r.pass_, r.unit, r.cta, r.sm, r.start_ns, r.end_ns))
+
+    cb = GIRIH_TRACE_FN(collect)
+    if trace:
+        opts.trace_cb = cb
+    led = None
+    if ledger and steps > 0:
+        led = np.zeros((steps, state.grid.nz, state.grid.ny, state.grid.nx), dtype=np.uint32)
+        opts.ledger = led.ctypes.data_as(C.POINTER(C.c_uint))
+    check(load().girih_gpu_run_ex(C.byref(v.view), int(steps), C.byref(cfg), C.byref(rep),
+                                  C.byref(opts)))
+    state.t_current = v.view.t_current
+    dt = np.dtype([("pass", "i4"), ("unit", "i4"), ("cta", "i4"), ("sm", "i4"),
+                   ("start_ns", "u8"), ("end_ns", "u8")])
+    return PerfReport.from_c(rep), np.array(recs, dtype=dt), led
 
 
 def nccl_unique_id() -> bytes:

@@ -141,6 +141,30 @@ def test_row_digest_matches_oracle(girih, oracle, slabs):
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_instrumented_run_ledger_and_trace(girih, oracle, kind):
+    # girih_gpu_run_ex (RunOptions): every (step, cell) update owned by exactly one unit, across
+    # fused depths, z chunks, emulated slabs and cluster variants; results still bitwise
+    g = girih
+    base = oracle.init_state(kind, 33, 47, 29, 1, 4, remap=True)
+    T = 7
+    ref = base.copy()
+    oracle.naive_sweep(ref, T)
+    cfgs = [g.GpuConfig(tb=tb) for tb in tbs_for(g, kind)]
+    cfgs += [g.GpuConfig(tb=max(tbs_for(g, kind)), zchunks=3, emulate_slabs=2)]
+    cfgs += [g.GpuConfig(tb=v["tb"], variant=v["index"]) for v in g.variants()
+             if v["kind"] == kind and v["cluster_y"] > 1]
+    for cfg in cfgs:
+        st = to_problem(g, base)
+        rep, trace, led = g.run_instrumented(st, T, cfg)
+        assert_state_equal(st, ref, f"instrumented {cfg}")
+        assert led.shape == (T, 29, 47, 33) and (led == 1).all(), f"ledger {cfg}: {np.unique(led)}"
+        assert len(trace) == rep.units > 0
+        assert (trace["end_ns"] >= trace["start_ns"]).all()
+        order = np.lexsort((trace["unit"], trace["pass"]))
+        assert (order == np.arange(len(trace))).all()
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_minimum_grid(girih, oracle, kind):
     # smallest admissible extents 2R+1 (stencil.cpp:61-63)
     g = girih
