@@ -165,6 +165,16 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
                       long long* first_index);
 
 /* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
+/* update_tile (proj/src/engine.cpp:294-330: one tile with a transient thread group, its
+ * dependencies complete). GPU counterpart: runs work units [unit_begin, unit_end) -- tile
+ * columns x z chunks -- of the single tb-step pass that advances the handle from t_current to
+ * t_current + tb. Units of one pass are independent (overlapped tiling), so a pass may be run in
+ * pieces, in any order; the state advances once every unit has run. *units_total receives the
+ * pass's unit count. A unit run twice is GIRIH_ESTATE (the scheduler's double completion,
+ * scheduler.cpp:66-69). Single-slab handles only. */
+int girih_gpu_update_units(void* handle, int tb, long long unit_begin, long long unit_end,
+                           long long* units_total);
+
 /* Instrumented drop-in call: the counterpart of the reference's RunOptions
  * (proj/include/girih/engine.hpp:100-103, engine.cpp:358-364, 413-416). One device, one launch
  * per pass. `trace_cb` receives one record per work unit (the GPU counterpart of the reference's

@@ -112,6 +112,8 @@ SIGNATURES = {
     "girih_gpu_download_coeffs": (C.c_int, [C.c_void_p, C.POINTER(_dp), C.c_int, _dp]),
     "girih_gpu_row_digest": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]),
     "girih_gpu_run_ex": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "girih_gpu_update_units": (C.c_int, [C.c_void_p, C.c_int, C.c_longlong, C.c_longlong,
+                                         C.POINTER(C.c_longlong)]),
     "girih_gpu_get_t": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "girih_gpu_set_config": (C.c_int, [C.c_void_p, C.POINTER(GirihGpuConfig)]),
     "girih_gpu_close": (C.c_int, [C.c_void_p]),

@@ -564,6 +564,13 @@ struct Handle {
         long long cap = 0, t_begin = 0;
         int npass = 0;
     } instr;
+    // girih_gpu_update_units: the pass being run piecewise (t0, depth, units already run)
+    struct UnitRun {
+        long long t0 = -1;
+        int tb = 0;
+        std::vector<char> done;
+        long long ndone = 0;
+    } urun;
 
     size_t plane_elems() const { return size_t(pitch) * Y; }
     size_t slab_elems(const Slab& s) const { return plane_elems() * s.Zloc; }
@@ -1171,6 +1178,8 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     p.nzc = tg.nzc;
     p.zc_len = tg.zc_len;
     p.units = tg.units;
+    p.unit0 = 0;
+    p.unit_n = tg.units;
     p.work = reinterpret_cast<int*>(s.work->p);
     p.ptrace = nullptr;
     if (std::getenv("GIRIH_TRACE")) {
@@ -2753,6 +2762,63 @@ int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_c
     });
     if (rc != GIRIH_OK && h) destroy(h);
     return rc;
+}
+
+int girih_gpu_update_units(void* handle, int tb, long long unit_begin, long long unit_end,
+                           long long* units_total) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (h.slabs.size() != 1 || h.nranks > 1)
+            throw_err(GIRIH_EINVAL, "girih_gpu_update_units needs a single-slab handle");
+        if (tb < 1 || tb > max_tb(h.kind)) throw_err(GIRIH_EINVAL, "fused step count out of range");
+        const std::vector<Pass> plan = make_plan(h.kind, h.t_current, tb, tb);
+        if (plan.size() != 1) throw_err(GIRIH_EINVAL, "no single pass of that depth from this level");
+        const Pass& ps = plan[0];
+        for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
+            if (b >= 2) ensure_scratch(h, b & 1);
+        const Variant* var =
+            select_variant(h.kind, tb, (h.cfg.tb == tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
+        if (var->tb != tb) var = select_variant(h.kind, tb, -1);
+        Slab& s = h.slabs[0];
+        GCHECK(cudaSetDevice(s.device));
+        LaunchInfo li;
+        PassParams p = build_params(h, ps, var, 0, h.t_current, &li);
+        if (h.urun.t0 != h.t_current || h.urun.tb != tb || h.urun.done.size() != size_t(p.units)) {
+            if (h.urun.ndone > 0)
+                throw_err(GIRIH_ESTATE, "a piecewise pass is still incomplete (run its other units first)");
+            h.urun = Handle::UnitRun{h.t_current, tb, std::vector<char>(size_t(p.units), 0), 0};
+        }
+        if (units_total) *units_total = p.units;
+        if (unit_begin < 0 || unit_end > p.units || unit_begin > unit_end)
+            throw_err(GIRIH_EINVAL, "unit range outside the pass");
+        // the reference's scheduler rejects a double completion (scheduler.cpp:66-69)
+        for (long long u = unit_begin; u < unit_end; ++u)
+            if (h.urun.done[size_t(u)]) throw_err(GIRIH_ESTATE, "work unit already run in this pass");
+        if (unit_end == unit_begin) return;
+        p.unit0 = int(unit_begin);
+        p.unit_n = int(unit_end - unit_begin);
+        p.work_base = 0;
+        GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+        const int max_grid = max_resident_ctas(var);
+        const int grid = std::min(p.unit_n * var->cy, max_grid / var->cy * var->cy);
+        const CUtensorMap& vmap = tensor_map(h, 0, s.buf[ps.src]->p, 1, var->lx, var->ly);
+        const CUtensorMap* cmap = &vmap;
+        const CUtensorMap* umap = &vmap;
+        if (h.nc > 0)
+            cmap = &tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc, var->aux_x, var->aux_y);
+        if (ps.src_prev >= 0)
+            umap = &tensor_map(h, 0, s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
+        const PassDesc pd = single_desc(h, 0, var, tb, p, vmap, *umap);
+        GCHECK(var->launch(*cmap, pd, p, grid, s.stream));
+        GCHECK(cudaStreamSynchronize(s.stream));
+        for (long long u = unit_begin; u < unit_end; ++u) h.urun.done[size_t(u)] = 1;
+        h.urun.ndone += unit_end - unit_begin;
+        if (h.urun.ndone == p.units) {  // the pass is complete: the state advances
+            h.t_current += tb;
+            h.urun = Handle::UnitRun{};
+            drop_graphs(h);
+        }
+    });
 }
 
 int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_passes, int* n_passes,

@@ -93,6 +93,7 @@ struct PassParams {
     int work_base;           // value of *work when this pass started (cumulative per step)
     int oz0;                 // local plane of the output store map's z = 0 (the slab's zout_lo)
     int units;               // tiles_x * tiles_y * nzc
+    int unit0, unit_n;       // single-pass launches run units [unit0, unit0 + unit_n)
     int* work;               // dynamic unit counter (zeroed before every launch)
     unsigned long long* ptrace;  // optional per-iteration phase clocks of CTA 0 (debug)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
@@ -313,7 +314,9 @@ __device__ __forceinline__ void cursor_set(Cursor& c, const PassParams& p, int t
     c.q = 0;
     if (u < total) {
         if (CHAIN) c.q = u / p.units;
-        c.ug = unit_geom(p, u - c.q * p.units);
+        // single passes may run a sub-range [unit0, unit0 + unit_n) of the pass's units
+        // (girih_gpu_update_units, the reference's update_tile)
+        c.ug = unit_geom(p, CHAIN ? u - c.q * p.units : u + p.unit0);
         c.n_it = (c.ug.zb - c.ug.za) + 2 * H;
     }
 }
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 
     // ---- producers (thread 0): V runs P elements ahead, aux PA elements ahead ----
     __shared__ int uq[UQ];
-    const int total = CHAIN ? cd.npass * p.units : p.units;  // units of the launch
+    const int total = CHAIN ? cd.npass * p.units : p.unit_n;  // units of the launch
     Cursor vcur{}, acur{};
     uint32_t vnext = G0, anext = G0;
     int drawn = 0;  // producer: next unit id, drawn one unit ahead
@@ -743,7 +746,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     for (int seq = 0;; ++seq) {
         const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
         if (u >= total) break;
-        const UnitGeom ug = unit_geom(p, CHAIN ? u % p.units : u);
+        const UnitGeom ug = unit_geom(p, CHAIN ? u % p.units : u + p.unit0);
         // chained: bit 0 = the unit's pass writes the penult level, bits 1.. = that pass
         int uflags = 0;
         if constexpr (CHAIN) {
@@ -1224,13 +1227,14 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             }
             if constexpr (CHAIN)
                 if (tid == STORE_TID && it == n_it - 1) pub_next = u;  // unit finished
-            if (INSTR && p.trace && tid == 0) {  // instrumentation: one record per unit
+            // instrumentation: one record per unit (a cluster's unit by its leader CTA)
+            if (INSTR && p.trace && tid == 0 && crank == 0) {
                 if (it == 0) unit_t0 = global_ns();
                 if (it == n_it - 1) {
                     const unsigned long long r = atomicAdd(p.trace_n, 1ull);
                     if ((long long)r < p.trace_cap) {
                         unsigned long long* rec = p.trace + 4 * r;
-                        rec[0] = ((unsigned long long)p.trace_pass << 32) | unsigned(u);
+                        rec[0] = ((unsigned long long)p.trace_pass << 32) | unsigned(u + p.unit0);
                         rec[1] = ((unsigned long long)blockIdx.x << 32) | sm_id();
                         rec[2] = unit_t0;
                         rec[3] = global_ns();

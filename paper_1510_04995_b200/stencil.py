@@ -411,6 +411,15 @@ class DeviceState:
         j, i = divmod(rem, arr.shape[2])
         return n.value, (i, j, k)
 
+    def update_units(self, tb: int, begin: int, end: int) -> int:
+        """update_tile (engine.cpp:294-330): runs work units [begin, end) of the single tb-step
+        pass from the current level (girih_gpu_update_units); the state advances by tb once every
+        unit of the pass has run. Returns the pass's unit count."""
+        n = C.c_longlong()
+        check(load().girih_gpu_update_units(self._handle(), int(tb), int(begin), int(end),
+                                            C.byref(n)))
+        return n.value
+
     def row_digest(self, field) -> int:
         """Device-side digest of a whole field ('u', 'v' or coefficient index c), ghosts and pad
         included: FNV-1a over the per-row FNV-1a hashes (girih_gpu_row_digest)."""
