@@ -104,6 +104,7 @@ typedef struct {
                                CTAs share the fused levels' halo rows through distributed
                                shared memory */
     int aux_prefetch;       /* coefficient planes fetched ahead */
+    int direct_out;         /* 1: output stored from registers (no smem staging + TMA store) */
 } girih_gpu_variant;
 
 const char* girih_gpu_last_error(void);
@@ -165,14 +166,16 @@ int girih_gpu_compare(void* handle, int field, const double* host, long long* n_
                       long long* first_index);
 
 /* Download coefficient fields (n pointers, may be NULL entries) and cc[5] (may be NULL). */
-/* update_tile (proj/src/engine.cpp:294-330: one tile with a transient thread group, its
- * dependencies complete). GPU counterpart: runs work units [unit_begin, unit_end) -- tile
- * columns x z chunks -- of the single tb-step pass that advances the handle from t_current to
- * t_current + tb. Units of one pass are independent (overlapped tiling), so a pass may be run in
- * pieces, in any order; the state advances once every unit has run. *units_total receives the
- * pass's unit count. A unit run twice is GIRIH_ESTATE (the scheduler's double completion,
- * scheduler.cpp:66-69). Single-slab handles only. */
-int girih_gpu_update_units(void* handle, int tb, long long unit_begin, long long unit_end,
+/* update_tile (proj/src/engine.cpp:294-330: one tile with a transient thread group, run by the
+ * caller once its dependency tiles are complete). GPU counterpart: runs work units
+ * [unit_begin, unit_end) of the plan that advances the handle by `steps` steps. Units are
+ * numbered pass-major over the plan's passes (*units_total receives the count); a unit is a tile
+ * column x z chunk of one pass. Units of one pass are independent (overlapped tiling) and may run
+ * in any order and in any pieces; a pass's units need every unit of the earlier passes complete
+ * (GIRIH_ESTATE otherwise, as is running a unit twice: the scheduler's double completion,
+ * scheduler.cpp:66-69). The state advances by `steps` once every unit has run. Single-slab
+ * handles only; the fused depth is the handle's configuration. */
+int girih_gpu_update_units(void* handle, long long steps, long long unit_begin, long long unit_end,
                            long long* units_total);
 
 /* Instrumented drop-in call: the counterpart of the reference's RunOptions

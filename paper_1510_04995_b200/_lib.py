@@ -60,7 +60,7 @@ class GirihGpuReport(C.Structure):
 class GirihGpuVariant(C.Structure):
     _fields_ = [("kind", C.c_int), ("tb", C.c_int), ("lx", C.c_int), ("ly", C.c_int),
                 ("threads", C.c_int), ("prefetch", C.c_int), ("smem_bytes", C.c_int),
-                ("cluster_y", C.c_int), ("aux_prefetch", C.c_int)]
+                ("cluster_y", C.c_int), ("aux_prefetch", C.c_int), ("direct_out", C.c_int)]
 
 
 class GirihGpuTraceRecord(C.Structure):
@@ -112,7 +112,7 @@ SIGNATURES = {
     "girih_gpu_download_coeffs": (C.c_int, [C.c_void_p, C.POINTER(_dp), C.c_int, _dp]),
     "girih_gpu_row_digest": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]),
     "girih_gpu_run_ex": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
-    "girih_gpu_update_units": (C.c_int, [C.c_void_p, C.c_int, C.c_longlong, C.c_longlong,
+    "girih_gpu_update_units": (C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong,
                                          C.POINTER(C.c_longlong)]),
     "girih_gpu_get_t": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "girih_gpu_set_config": (C.c_int, [C.c_void_p, C.POINTER(GirihGpuConfig)]),

@@ -566,8 +566,10 @@ struct Handle {
     } instr;
     // girih_gpu_update_units: the pass being run piecewise (t0, depth, units already run)
     struct UnitRun {
-        long long t0 = -1;
+        long long t0 = -1, steps = 0;
         int tb = 0;
+        std::vector<Pass> plan;
+        std::vector<long long> base;  // first unit of each pass (+ the total)
         std::vector<char> done;
         long long ndone = 0;
     } urun;
@@ -2291,6 +2293,7 @@ int girih_gpu_variant_info(int index, girih_gpu_variant* out) {
         out->smem_bytes = v->smem_bytes;
         out->cluster_y = v->cy;
         out->aux_prefetch = v->aux_prefetch;
+        out->direct_out = v->direct_out;
     });
 }
 
@@ -2672,6 +2675,181 @@ int girih_gpu_run(girih_state_view* state, long long steps, const girih_gpu_conf
     });
     if (rc != GIRIH_OK && h) destroy(h);
     return rc;
+}
+
+int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
+                     girih_gpu_report* report, girih_gpu_run_options* opts) {
+    if (!opts || (!opts->ledger && !opts->trace_cb)) return girih_gpu_run(state, steps, cfg, report);
+    Handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!state) throw_err(GIRIH_EINVAL, "null argument");
+        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
+        {
+            Handle probe;
+            setup_geometry(probe, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        }
+        opts->trace_total = 0;
+        if (steps == 0) {
+            if (report) std::memset(report, 0, sizeof *report);
+            return;
+        }
+        girih_gpu_config c = cfg ? *cfg : default_config();
+        if (c.ngpus > 1)
+            throw_err(GIRIH_EINVAL, "instrumented runs use one device (emulated slabs allowed)");
+        c.chain = -1;   // one launch per pass: every unit belongs to one pass
+        c.graphs = -1;
+        const auto w0 = std::chrono::steady_clock::now();
+        h = new Handle();
+        h->uploads_all = true;
+        h->cfg = c;
+        setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
+        validate_config(h->cfg, h->kind);
+        setup_slabs(*h);
+        upload_state(*h, *state);
+        Slab& s0 = h->slabs[0];
+        const size_t cells = size_t(h->nx) * h->ny * h->nz;
+        h->instr.on = true;
+        h->instr.t_begin = state->t_current;
+        if (opts->ledger) {
+            alloc_buf(h->instr.ledger, s0.device, (size_t(steps) * cells + 1) / 2, s0.stream);
+        }
+        if (opts->trace_cb) {
+            h->instr.cap = opts->trace_capacity > 0 ? opts->trace_capacity : (1ll << 20);
+            alloc_buf(h->instr.trace, s0.device, size_t(h->instr.cap) * 4 + 1, s0.stream);
+        }
+        girih_gpu_report r{};
+        step_timed(*h, steps, &r);
+        std::vector<double*> d(h->slabs.size());
+        for (int f = 0; f < 2; ++f) {
+            for (size_t g = 0; g < h->slabs.size(); ++g) d[g] = h->slabs[g].buf[f]->p;
+            copy_d2h(*h, d.data(), f == 0 ? state->u : state->v);
+        }
+        GCHECK(cudaSetDevice(s0.device));
+        if (opts->ledger)
+            GCHECK(cudaMemcpyAsync(opts->ledger, h->instr.ledger->p, size_t(steps) * cells * 4,
+                                   cudaMemcpyDeviceToHost, s0.stream));
+        std::vector<unsigned long long> raw;
+        unsigned long long n = 0;
+        if (opts->trace_cb) {
+            const auto* tp = reinterpret_cast<const unsigned long long*>(h->instr.trace->p);
+            GCHECK(cudaMemcpyAsync(&n, tp + 4 * h->instr.cap, 8, cudaMemcpyDeviceToHost, s0.stream));
+            GCHECK(cudaStreamSynchronize(s0.stream));
+            raw.resize(size_t(std::min<long long>((long long)n, h->instr.cap)) * 4);
+            GCHECK(cudaMemcpyAsync(raw.data(), tp, raw.size() * 8, cudaMemcpyDeviceToHost, s0.stream));
+        }
+        sync_all(*h);
+        state->t_current = h->t_current;
+        if (opts->trace_cb) {
+            std::vector<girih_gpu_trace_record> recs(raw.size() / 4);
+            for (size_t q = 0; q < recs.size(); ++q) {
+                recs[q].pass = int(raw[4 * q] >> 32);
+                recs[q].unit = int(raw[4 * q] & 0xffffffffu);
+                recs[q].cta = int(raw[4 * q + 1] >> 32);
+                recs[q].sm = int(raw[4 * q + 1] & 0xffffffffu);
+                recs[q].start_ns = raw[4 * q + 2];
+                recs[q].end_ns = raw[4 * q + 3];
+            }
+            std::sort(recs.begin(), recs.end(), [](const auto& a, const auto& b) {
+                return a.pass != b.pass ? a.pass < b.pass : a.unit < b.unit;
+            });
+            opts->trace_total = (long long)n;
+            opts->trace_cb(opts->trace_ctx, recs.data(), (long long)recs.size());
+        }
+        if (report) {
+            *report = r;
+            report->wall_s =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+        }
+        destroy(h);
+        h = nullptr;
+    });
+    if (rc != GIRIH_OK && h) destroy(h);
+    return rc;
+}
+
+int girih_gpu_update_units(void* handle, long long steps, long long unit_begin,
+                           long long unit_end, long long* units_total) {
+    return guarded([&] {
+        Handle& h = *as_handle(handle);
+        if (h.slabs.size() != 1 || h.nranks > 1)
+            throw_err(GIRIH_EINVAL, "girih_gpu_update_units needs a single-slab handle");
+        if (steps < 1) throw_err(GIRIH_EINVAL, "step count must be positive");
+        Handle::UnitRun& ur = h.urun;
+        const int tb = h.cfg.tb > 0 ? h.cfg.tb : default_tb_for(h);
+        if (ur.t0 != h.t_current || ur.steps != steps || ur.tb != tb) {
+            if (ur.ndone > 0)
+                throw_err(GIRIH_ESTATE, "a piecewise run is incomplete (run its remaining units first)");
+            // the plan of `steps` steps and the unit ranges of its passes, numbered pass-major
+            ur = Handle::UnitRun{};
+            ur.t0 = h.t_current;
+            ur.steps = steps;
+            ur.tb = tb;
+            ur.plan = make_plan(h.kind, h.t_current, steps, tb);
+            long long t = h.t_current, base = 0;
+            for (const Pass& ps : ur.plan) {
+                for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
+                    if (b >= 2) ensure_scratch(h, b & 1);
+                const Variant* var = select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
+                if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+                LaunchInfo li;
+                const PassParams p = build_params(h, ps, var, 0, t, &li);
+                ur.base.push_back(base);
+                base += p.units;
+                t += ps.tb;
+            }
+            ur.base.push_back(base);
+            ur.done.assign(size_t(base), 0);
+        }
+        const long long total = ur.base.back();
+        if (units_total) *units_total = total;
+        if (unit_begin < 0 || unit_end > total || unit_begin > unit_end)
+            throw_err(GIRIH_EINVAL, "unit range outside the run");
+        // the reference's scheduler rejects a double completion (scheduler.cpp:66-69)
+        for (long long u = unit_begin; u < unit_end; ++u)
+            if (ur.done[size_t(u)]) throw_err(GIRIH_ESTATE, "work unit already run");
+        Slab& s = h.slabs[0];
+        GCHECK(cudaSetDevice(s.device));
+        long long t = ur.t0;
+        for (size_t q = 0; q < ur.plan.size(); ++q) {
+            const Pass& ps = ur.plan[q];
+            const long long a = std::max(unit_begin, ur.base[q]), e = std::min(unit_end, ur.base[q + 1]);
+            if (a < e) {
+                // every unit of the earlier passes must be complete (they write what this reads)
+                for (long long u = 0; u < ur.base[q]; ++u)
+                    if (!ur.done[size_t(u)])
+                        throw_err(GIRIH_ESTATE, "units of an earlier pass are not complete");
+                const Variant* var = select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
+                if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+                LaunchInfo li;
+                PassParams p = build_params(h, ps, var, 0, t, &li);
+                p.unit0 = int(a - ur.base[q]);
+                p.unit_n = int(e - a);
+                p.work_base = 0;
+                GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+                const int max_grid = max_resident_ctas(var);
+                const int grid = std::min(p.unit_n * var->cy, max_grid / var->cy * var->cy);
+                const CUtensorMap& vmap = tensor_map(h, 0, s.buf[ps.src]->p, 1, var->lx, var->ly);
+                const CUtensorMap* cmap = &vmap;
+                const CUtensorMap* umap = &vmap;
+                if (h.nc > 0)
+                    cmap = &tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc,
+                                       var->aux_x, var->aux_y);
+                if (ps.src_prev >= 0)
+                    umap = &tensor_map(h, 0, s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
+                const PassDesc pd = single_desc(h, 0, var, ps.tb, p, vmap, *umap);
+                GCHECK(var->launch(*cmap, pd, p, grid, s.stream));
+                GCHECK(cudaStreamSynchronize(s.stream));
+                for (long long u = a; u < e; ++u) ur.done[size_t(u)] = 1;
+                ur.ndone += e - a;
+            }
+            t += ps.tb;
+        }
+        if (ur.ndone == total) {  // every unit of every pass has run: the state advances
+            h.t_current = ur.t0 + steps;
+            ur = Handle::UnitRun{};
+            drop_graphs(h);
+        }
+    });
 }
 
 int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_config* cfg,

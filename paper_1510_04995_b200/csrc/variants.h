@@ -24,6 +24,7 @@ struct Variant {
     LaunchChainFn launch_chain;  // cd.npass chained passes over the same tile grid (cy == 1)
     OccFn occupancy;             // resident CTAs, single-pass kernel (a multiple of cy)
     OccFn occupancy_chain;       // the same for the chained kernel
+    int direct_out;              // 1: output level stored straight from registers (no staging)
 };
 
 // one table per kind, defined in variants_<kind>.cu
@@ -36,12 +37,13 @@ extern const int kNumVariantsConst25;
 extern const Variant kVariantsVar25[];
 extern const int kNumVariantsVar25;
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY,
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CF,
           bool INSTR = false>
 cudaError_t launch_zwave_impl(const CUtensorMap& cmap, const ChainDescs& cd, const PassParams& p,
                               int grid, cudaStream_t stream) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
-    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY, INSTR>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>;
+    constexpr int CY = CFG::CY;
+    auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CF, INSTR>;
     // once per instantiation (thread-safe static initialisation)
     static const cudaError_t attr =
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
@@ -72,18 +74,18 @@ cudaError_t launch_zwave_impl(const CUtensorMap& cmap, const ChainDescs& cd, con
     return cudaGetLastError();
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CF>
 cudaError_t launch_zwave_chain(const CUtensorMap& cmap, const ChainDescs& cd, const PassParams& p,
                                int grid, cudaStream_t stream) {
-    if constexpr (CY > 1) {
+    if constexpr ((CF & 255) > 1) {
         return cudaErrorNotSupported;  // cluster kernels run single passes
     } else {
-        return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, true, 1>(cmap, cd, p, grid, stream);
+        return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, true, CF>(cmap, cd, p, grid, stream);
     }
 }
 
 // one pass = a chain of length 1 (no dependency flags)
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY, bool INSTR = false>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CF, bool INSTR = false>
 cudaError_t launch_zwave(const CUtensorMap& cmap, const PassDesc& d, const PassParams& p, int grid,
                          cudaStream_t stream) {
     ChainDescs cd{};
@@ -91,18 +93,19 @@ cudaError_t launch_zwave(const CUtensorMap& cmap, const PassDesc& d, const PassP
     cd.pidx[0] = 0;
     cd.npass = 1;
     cd.done = nullptr;
-    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false, CY, INSTR>(cmap, cd, p, grid,
+    return launch_zwave_impl<KIND, TB, LX, LY, NT, P, PA, MINB, false, CF, INSTR>(cmap, cd, p, grid,
                                                                                    stream);
 }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CY, bool CHAIN = false>
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, int CF, bool CHAIN = false>
 cudaError_t occupancy_zwave(int* max_ctas) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>;
+    constexpr int CY = CFG::CY;
     *max_ctas = 0;
     if constexpr (CHAIN && CY > 1) {
         return cudaSuccess;  // not launchable chained
     } else {
-        auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CY>;
+        auto* fn = zwave_kernel<KIND, TB, LX, LY, NT, P, PA, MINB, CHAIN, CF>;
         cudaError_t e =
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CFG::SMEM));
         if (e != cudaSuccess) return e;
@@ -139,20 +142,27 @@ cudaError_t occupancy_zwave(int* max_ctas) {
     }
 }
 
-#define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY)                                \
+#define GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, CF)                                \
     Variant {                                                                                 \
-        KIND, TB, LX, LY, NT, P, PA, MINB, CY,                                                \
-            int(ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::SMEM),                    \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AXO,                          \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AYO,                          \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AX,                           \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>::AY,                           \
-            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                             \
-            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY, true>,                       \
-            &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                       \
-            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY>,                          \
-            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CY, true>                     \
+        KIND, TB, LX, LY, NT, P, PA, MINB, (CF) & 255,                                        \
+            int(ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::SMEM),                    \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::AXO,                          \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::AYO,                          \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::AX,                           \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::AY,                           \
+            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                             \
+            &launch_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF, true>,                       \
+            &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                       \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                          \
+            &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF, true>,                    \
+            ((CF) >> 8) & 1                                                                   \
     }
+// CY CTAs per y cluster
+#define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \
+    GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, CY)
+// direct output stores (no staging planes)
+#define GIRIH_VARIANT_D(KIND, TB, LX, LY, NT, P, PA, MINB) \
+    GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, 1 | (1 << 8))
 #define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB) \
     GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, 1)
 

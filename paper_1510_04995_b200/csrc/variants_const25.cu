@@ -14,6 +14,7 @@ const Variant kVariantsConst25[] = {
     GIRIH_VARIANT(K_CONST25, 2, 32, 32, 192, 2, 1, 1),
     GIRIH_VARIANT_C(K_CONST25, 2, 64, 20, 192, 1, 1, 1, 4),
     GIRIH_VARIANT_C(K_CONST25, 2, 64, 16, 128, 1, 1, 1, 8),
+    GIRIH_VARIANT_D(K_CONST25, 1, 64, 40, 256, 1, 1, 1),
 };
 const int kNumVariantsConst25 = sizeof(kVariantsConst25) / sizeof(kVariantsConst25[0]);
 

@@ -15,6 +15,7 @@ const Variant kVariantsConst7[] = {
     GIRIH_VARIANT_C(K_CONST7, 2, 64, 18, 256, 3, 0, 2, 4),
     GIRIH_VARIANT_C(K_CONST7, 3, 64, 32, 480, 3, 0, 1, 4),
     GIRIH_VARIANT_C(K_CONST7, 4, 64, 32, 480, 2, 0, 1, 4),
+    GIRIH_VARIANT_D(K_CONST7, 1, 64, 10, 128, 4, 0, 5),
 };
 const int kNumVariantsConst7 = sizeof(kVariantsConst7) / sizeof(kVariantsConst7[0]);
 

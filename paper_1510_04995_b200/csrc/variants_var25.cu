@@ -7,6 +7,7 @@ namespace girih_gpu {
 const Variant kVariantsVar25[] = {
     GIRIH_VARIANT(K_VAR25, 1, 32, 16, 64, 1, 1, 2),
     GIRIH_VARIANT(K_VAR25, 1, 32, 32, 128, 2, 1, 1),
+    GIRIH_VARIANT_D(K_VAR25, 1, 32, 16, 64, 1, 1, 2),
 };
 const int kNumVariantsVar25 = sizeof(kVariantsVar25) / sizeof(kVariantsVar25[0]);
 

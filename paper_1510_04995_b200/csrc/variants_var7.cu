@@ -25,6 +25,9 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 256, 2, 1, 1, 4),
     GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 256, 2, 1, 1, 8),
     GIRIH_VARIANT_C(K_VAR7, 4, 64, 10, 128, 2, 1, 1, 4),
+    GIRIH_VARIANT_D(K_VAR7, 2, 64, 18, 512, 2, 1, 1),
+    GIRIH_VARIANT_D(K_VAR7, 2, 64, 18, 512, 2, 2, 1),
+    GIRIH_VARIANT_D(K_VAR7, 2, 64, 17, 480, 2, 2, 1),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

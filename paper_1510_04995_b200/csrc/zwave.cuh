@@ -412,8 +412,13 @@ template <> struct AuxArrays<K_CONST25> { static constexpr int N = 2; };  // C a
 
 constexpr int round16(int n) { return (n + 15) / 16 * 16; }
 
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1, int CY = 1>
+// CF = cluster rows CY (bits 0-7) | flags << 8. Flag 1: DOUT, the output level is stored from
+// registers straight to global memory (coalesced pair stores) instead of an smem staging plane
+// and a TMA store, which frees the staging planes' shared memory for deeper prefetch.
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB = 1, int CF = 1>
 struct ZwaveConfig {
+    static constexpr int CY = CF & 255;
+    static constexpr bool DOUT = ((CF >> 8) & 1) != 0;
     static constexpr int R = KindTraits<KIND>::R;
     static constexpr int Q = 2 * R + 1;     // z window of one level
     // z neighbours come from per-thread register queues; smem only holds the centre planes
@@ -458,7 +463,7 @@ struct ZwaveConfig {
     static constexpr int AUXPLANE = NAUX * AYX;
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
     static constexpr int GUARD = round16(LX * R + R + 8);
-    static constexpr int STAGE = round16(OXM * OYS);  // one output staging plane
+    static constexpr int STAGE = DOUT ? 0 : round16(OXM * OYS);  // one output staging plane
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
                                            size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
@@ -478,13 +483,15 @@ struct ZwaveConfig {
 // CHAIN = false: one pass (descriptors d[0]); true: cd.npass chained passes. The two are
 // separate instantiations so that single-pass launches carry none of the chaining state (the
 // 128-register var7pt CTA spills otherwise, and shared-memory producer state cost 30%).
-template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CY = 1,
+template <int KIND, int TB, int LX, int LY, int NT, int P, int PA, int MINB, bool CHAIN, int CF = 1,
           bool INSTR = false>
 __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 1) ? MINB - 1 : MINB)
     zwave_kernel(const __grid_constant__ CUtensorMap cmap,  // coefficient block (4-D)
                  const __grid_constant__ ChainDescs cd,     // per-pass buffers and maps
                  const __grid_constant__ PassParams p) {
-    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CY>;
+    using CFG = ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>;
+    constexpr int CY = CFG::CY;
+    constexpr bool DOUT = CFG::DOUT;
     static_assert(CY == 1 || !CHAIN, "cluster kernels run single passes");
     static_assert(!INSTR || !CHAIN, "instrumented kernels run single passes");
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
@@ -1084,13 +1091,30 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         newest[i] = val[i];
                     }
                 } else if (k >= ug.za && k < ug.zb) {
+                    if constexpr (DOUT) {
+                        // straight to global memory: interior output cells only (the TMA store
+                        // map's clipping, done by the masks); a full pair is one aligned
+                        // 16-byte store (x pair origins are even, off + R is even)
+                        double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
+#pragma unroll
+                        for (int i = 0; i < PPT; ++i) {
+                            const uint32_t m = ((out_mask & ~ghost_mask) >> (2 * i)) & 3u;
+                            if (m == 3u) {
+                                *reinterpret_cast<double2*>(dst + colidx[2 * i]) = val[i];
+                            } else {
+                                if (m & 1u) dst[colidx[2 * i]] = val[i].x;
+                                if (m & 2u) dst[colidx[2 * i + 1]] = val[i].y;
+                            }
+                        }
+                    } else {
                     double* stg = stage + (g % 3) * STAGE;
 #pragma unroll
                     for (int i = 0; i < PPT; ++i) {
                         if ((out_mask >> (2 * i)) & 1) stg[sidx[i]] = val[i].x;  // clipped by omap
                         if ((out_mask >> (2 * i + 1)) & 1) stg[sidx[i] + 1] = val[i].y;
                     }
-                    if (any_odd_col && k >= p.zout_lo && k < p.zout_hi) {
+                    }
+                    if (!DOUT && any_odd_col && k >= p.zout_lo && k < p.zout_hi) {
                         double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
 #pragma unroll
                         for (int i = 0; i < PPT; ++i) {
@@ -1155,7 +1179,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                             }
                         }
                     }
-                    staged = true;
+                    staged = !DOUT;
                 }
             }
             if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC)

@@ -154,7 +154,7 @@ def variants():
         check(lib.girih_gpu_variant_info(i, C.byref(v)))
         out.append(dict(index=i, kind=v.kind, tb=v.tb, lx=v.lx, ly=v.ly, threads=v.threads,
                         prefetch=v.prefetch, smem_bytes=v.smem_bytes, cluster_y=v.cluster_y,
-                        aux_prefetch=v.aux_prefetch))
+                        aux_prefetch=v.aux_prefetch, direct_out=v.direct_out))
     return out
 
 
@@ -411,12 +411,12 @@ class DeviceState:
         j, i = divmod(rem, arr.shape[2])
         return n.value, (i, j, k)
 
-    def update_units(self, tb: int, begin: int, end: int) -> int:
-        """update_tile (engine.cpp:294-330): runs work units [begin, end) of the single tb-step
-        pass from the current level (girih_gpu_update_units); the state advances by tb once every
-        unit of the pass has run. Returns the pass's unit count."""
+    def update_units(self, steps: int, begin: int, end: int) -> int:
+        """update_tile (engine.cpp:294-330): runs work units [begin, end) -- numbered pass-major
+        over the plan that advances the state by `steps` -- (girih_gpu_update_units); the state
+        advances once every unit has run. Returns the plan's unit count."""
         n = C.c_longlong()
-        check(load().girih_gpu_update_units(self._handle(), int(tb), int(begin), int(end),
+        check(load().girih_gpu_update_units(self._handle(), int(steps), int(begin), int(end),
                                             C.byref(n)))
         return n.value
 

@@ -166,31 +166,34 @@ def test_instrumented_run_ledger_and_trace(girih, oracle, kind):
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_update_units_piecewise_passes(girih, oracle, kind):
-    # update_tile counterpart: every pass run as shuffled pieces of its work units (any order)
-    # equals the oracle; a unit run twice is refused like the scheduler's double completion
+    # update_tile counterpart: each pass of a plan run as shuffled pieces of its work units (any
+    # order within a pass) equals the oracle; a unit run twice, or a unit of a later pass before
+    # the earlier pass is complete, is refused like the reference scheduler's misuse errors
     g = girih
     rng = np.random.default_rng(kind)
     base = oracle.init_state(kind, 45, 38, 27, 1, 8, remap=True)
-    tbmax = max(tbs_for(g, kind))
-    steps = 0
+    done_steps = 0
     with g.DeviceState.seeded(kind, g.GridSpec(45, 38, 27, 1), 8, remap=True,
-                              config=g.GpuConfig(zchunks=3)) as ds:
-        for tb in (tbmax, 1, tbmax):
-            n = ds.update_units(tb, 0, 0)
+                              config=g.GpuConfig(zchunks=3, tb=max(tbs_for(g, kind)))) as ds:
+        for steps in (5, 2):
+            n = ds.update_units(steps, 0, 0)
             assert n > 1
-            cuts = sorted(set(rng.integers(1, n, size=min(4, n - 1)).tolist()))
-            pieces = list(zip([0] + cuts, cuts + [n]))
-            rng.shuffle(pieces)
-            for a, b in pieces[:-1]:
-                ds.update_units(tb, a, b)
             with pytest.raises(g.GirihError):
-                ds.update_units(tb, pieces[0][0], pieces[0][1])  # already run
-            assert ds.t_current == steps
-            ds.update_units(tb, *pieces[-1])
-            steps += tb
-            assert ds.t_current == steps
+                ds.update_units(steps, n - 1, n)  # last pass before the first is complete
+            # two single-unit pieces out of order (both in the first pass), then random pieces
+            cuts = sorted(set([1, 2] + rng.integers(3, n, size=min(6, max(0, n - 3))).tolist()))
+            pieces = list(zip([0] + cuts, cuts + [n]))
+            order = [pieces[1], pieces[0]] + pieces[2:]
+            for a, b in order[:-1]:
+                ds.update_units(steps, a, b)
+            with pytest.raises(g.GirihError):
+                ds.update_units(steps, order[0][0], order[0][1])  # already run
+            assert ds.t_current == done_steps
+            ds.update_units(steps, *order[-1])
+            done_steps += steps
+            assert ds.t_current == done_steps
         ref = base.copy()
-        oracle.naive_sweep(ref, steps)
+        oracle.naive_sweep(ref, done_steps)
         got = ds.download()
     assert_state_equal(got, ref, "piecewise passes")
 

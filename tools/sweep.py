@@ -22,11 +22,13 @@ ap.add_argument("--variants", default="all")
 ap.add_argument("--zchunks", default="0", help="comma list of z-chunk counts (0 = model)")
 ap.add_argument("--tbs", default="", help="comma list of fused depths to sweep (default all)")
 ap.add_argument("--clusters", default="all", choices=["all", "only", "none"])
+ap.add_argument("--variants-list", default="", help="comma list of global variant indices")
 a = ap.parse_args()
 for kind in [int(k) for k in a.kinds.split(",")]:
     vs = [v for v in g.variants() if v["kind"] == kind and
           (not a.tbs or v["tb"] in [int(t) for t in a.tbs.split(",")]) and
-          (a.clusters == "all" or (v["cluster_y"] > 1) == (a.clusters == "only"))]
+          (a.clusters == "all" or (v["cluster_y"] > 1) == (a.clusters == "only")) and
+          (not a.variants_list or v["index"] in [int(x) for x in a.variants_list.split(",")])]
     grid = g.GridSpec(a.n, a.n, a.n, 0)
     with g.DeviceState.seeded(kind, grid, 42, remap=True) as ds:
         for v, zc in [(v, int(z)) for v in vs for z in a.zchunks.split(",")]:
@@ -40,7 +42,8 @@ for kind in [int(k) for k in a.kinds.split(",")]:
             avg = best.pass_seconds / best.n_launches
             print(json.dumps({"kind": g.KINDS[kind], "n": a.n, "tb": v["tb"], "variant": v["index"],
                               "lx": v["lx"], "ly": v["ly"], "threads": v["threads"],
-                              "cy": v["cluster_y"], "mlups": round(best.mlups),
+                              "cy": v["cluster_y"], "p": v["prefetch"], "pa": v["aux_prefetch"],
+                              "dout": v["direct_out"], "mlups": round(best.mlups),
                               "avg_pass_ms": round(avg * 1e3, 4), "passes": best.n_launches,
                               "eff_GBs": round(a.n ** 3 * B1[kind] / avg / 1e9, 1),
                               "zchunks": best.zchunks_used, "grid": best.grid_ctas,
