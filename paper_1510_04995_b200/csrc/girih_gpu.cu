@@ -2852,153 +2852,6 @@ int girih_gpu_update_units(void* handle, long long steps, long long unit_begin,
     });
 }
 
-int girih_gpu_run_ex(girih_state_view* state, long long steps, const girih_gpu_config* cfg,
-                     girih_gpu_report* report, girih_gpu_run_options* opts) {
-    if (!opts || (!opts->ledger && !opts->trace_cb)) return girih_gpu_run(state, steps, cfg, report);
-    Handle* h = nullptr;
-    const int rc = guarded([&] {
-        if (!state) throw_err(GIRIH_EINVAL, "null argument");
-        if (steps < 0) throw_err(GIRIH_EINVAL, "negative step count");
-        {
-            Handle probe;
-            setup_geometry(probe, state->kind, state->nx, state->ny, state->nz, state->pad_x);
-        }
-        opts->trace_total = 0;
-        if (steps == 0) {
-            if (report) std::memset(report, 0, sizeof *report);
-            return;
-        }
-        girih_gpu_config c = cfg ? *cfg : default_config();
-        if (c.ngpus > 1)
-            throw_err(GIRIH_EINVAL, "instrumented runs use one device (emulated slabs allowed)");
-        c.chain = -1;   // one launch per pass: every unit belongs to one pass
-        c.graphs = -1;
-        const auto w0 = std::chrono::steady_clock::now();
-        h = new Handle();
-        h->uploads_all = true;
-        h->cfg = c;
-        setup_geometry(*h, state->kind, state->nx, state->ny, state->nz, state->pad_x);
-        validate_config(h->cfg, h->kind);
-        setup_slabs(*h);
-        upload_state(*h, *state);
-        Slab& s0 = h->slabs[0];
-        const size_t cells = size_t(h->nx) * h->ny * h->nz;
-        h->instr.on = true;
-        h->instr.t_begin = state->t_current;
-        if (opts->ledger) {
-            alloc_buf(h->instr.ledger, s0.device, (size_t(steps) * cells + 1) / 2, s0.stream);
-        }
-        if (opts->trace_cb) {
-            h->instr.cap = opts->trace_capacity > 0 ? opts->trace_capacity : (1ll << 20);
-            alloc_buf(h->instr.trace, s0.device, size_t(h->instr.cap) * 4 + 1, s0.stream);
-        }
-        girih_gpu_report r{};
-        step_timed(*h, steps, &r);
-        std::vector<double*> d(h->slabs.size());
-        for (int f = 0; f < 2; ++f) {
-            for (size_t g = 0; g < h->slabs.size(); ++g) d[g] = h->slabs[g].buf[f]->p;
-            copy_d2h(*h, d.data(), f == 0 ? state->u : state->v);
-        }
-        GCHECK(cudaSetDevice(s0.device));
-        if (opts->ledger)
-            GCHECK(cudaMemcpyAsync(opts->ledger, h->instr.ledger->p, size_t(steps) * cells * 4,
-                                   cudaMemcpyDeviceToHost, s0.stream));
-        std::vector<unsigned long long> raw;
-        unsigned long long n = 0;
-        if (opts->trace_cb) {
-            const auto* tp = reinterpret_cast<const unsigned long long*>(h->instr.trace->p);
-            GCHECK(cudaMemcpyAsync(&n, tp + 4 * h->instr.cap, 8, cudaMemcpyDeviceToHost, s0.stream));
-            GCHECK(cudaStreamSynchronize(s0.stream));
-            raw.resize(size_t(std::min<long long>((long long)n, h->instr.cap)) * 4);
-            GCHECK(cudaMemcpyAsync(raw.data(), tp, raw.size() * 8, cudaMemcpyDeviceToHost, s0.stream));
-        }
-        sync_all(*h);
-        state->t_current = h->t_current;
-        if (opts->trace_cb) {
-            std::vector<girih_gpu_trace_record> recs(raw.size() / 4);
-            for (size_t q = 0; q < recs.size(); ++q) {
-                recs[q].pass = int(raw[4 * q] >> 32);
-                recs[q].unit = int(raw[4 * q] & 0xffffffffu);
-                recs[q].cta = int(raw[4 * q + 1] >> 32);
-                recs[q].sm = int(raw[4 * q + 1] & 0xffffffffu);
-                recs[q].start_ns = raw[4 * q + 2];
-                recs[q].end_ns = raw[4 * q + 3];
-            }
-            std::sort(recs.begin(), recs.end(), [](const auto& a, const auto& b) {
-                return a.pass != b.pass ? a.pass < b.pass : a.unit < b.unit;
-            });
-            opts->trace_total = (long long)n;
-            opts->trace_cb(opts->trace_ctx, recs.data(), (long long)recs.size());
-        }
-        if (report) {
-            *report = r;
-            report->wall_s =
-                std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
-        }
-        destroy(h);
-        h = nullptr;
-    });
-    if (rc != GIRIH_OK && h) destroy(h);
-    return rc;
-}
-
-int girih_gpu_update_units(void* handle, int tb, long long unit_begin, long long unit_end,
-                           long long* units_total) {
-    return guarded([&] {
-        Handle& h = *as_handle(handle);
-        if (h.slabs.size() != 1 || h.nranks > 1)
-            throw_err(GIRIH_EINVAL, "girih_gpu_update_units needs a single-slab handle");
-        if (tb < 1 || tb > max_tb(h.kind)) throw_err(GIRIH_EINVAL, "fused step count out of range");
-        const std::vector<Pass> plan = make_plan(h.kind, h.t_current, tb, tb);
-        if (plan.size() != 1) throw_err(GIRIH_EINVAL, "no single pass of that depth from this level");
-        const Pass& ps = plan[0];
-        for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
-            if (b >= 2) ensure_scratch(h, b & 1);
-        const Variant* var =
-            select_variant(h.kind, tb, (h.cfg.tb == tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
-        if (var->tb != tb) var = select_variant(h.kind, tb, -1);
-        Slab& s = h.slabs[0];
-        GCHECK(cudaSetDevice(s.device));
-        LaunchInfo li;
-        PassParams p = build_params(h, ps, var, 0, h.t_current, &li);
-        if (h.urun.t0 != h.t_current || h.urun.tb != tb || h.urun.done.size() != size_t(p.units)) {
-            if (h.urun.ndone > 0)
-                throw_err(GIRIH_ESTATE, "a piecewise pass is still incomplete (run its other units first)");
-            h.urun = Handle::UnitRun{h.t_current, tb, std::vector<char>(size_t(p.units), 0), 0};
-        }
-        if (units_total) *units_total = p.units;
-        if (unit_begin < 0 || unit_end > p.units || unit_begin > unit_end)
-            throw_err(GIRIH_EINVAL, "unit range outside the pass");
-        // the reference's scheduler rejects a double completion (scheduler.cpp:66-69)
-        for (long long u = unit_begin; u < unit_end; ++u)
-            if (h.urun.done[size_t(u)]) throw_err(GIRIH_ESTATE, "work unit already run in this pass");
-        if (unit_end == unit_begin) return;
-        p.unit0 = int(unit_begin);
-        p.unit_n = int(unit_end - unit_begin);
-        p.work_base = 0;
-        GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
-        const int max_grid = max_resident_ctas(var);
-        const int grid = std::min(p.unit_n * var->cy, max_grid / var->cy * var->cy);
-        const CUtensorMap& vmap = tensor_map(h, 0, s.buf[ps.src]->p, 1, var->lx, var->ly);
-        const CUtensorMap* cmap = &vmap;
-        const CUtensorMap* umap = &vmap;
-        if (h.nc > 0)
-            cmap = &tensor_map(h, 0, s.cblock->p, h.kind == K_CONST25 ? 1 : h.nc, var->aux_x, var->aux_y);
-        if (ps.src_prev >= 0)
-            umap = &tensor_map(h, 0, s.buf[ps.src_prev]->p, 1, var->aux_x, var->aux_y);
-        const PassDesc pd = single_desc(h, 0, var, tb, p, vmap, *umap);
-        GCHECK(var->launch(*cmap, pd, p, grid, s.stream));
-        GCHECK(cudaStreamSynchronize(s.stream));
-        for (long long u = unit_begin; u < unit_end; ++u) h.urun.done[size_t(u)] = 1;
-        h.urun.ndone += unit_end - unit_begin;
-        if (h.urun.ndone == p.units) {  // the pass is complete: the state advances
-            h.t_current += tb;
-            h.urun = Handle::UnitRun{};
-            drop_graphs(h);
-        }
-    });
-}
-
 int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_passes, int* n_passes,
                    int* pass_tb, int* pass_src, int* pass_src_prev, int* pass_dst,
                    int* pass_dst_penult) {
@@ -3017,6 +2870,53 @@ int girih_gpu_plan(int kind, long long t0, long long steps, int tb, int max_pass
         }
     });
 }
+
+namespace {
+// The GPU counterpart of the reference's analytic models (models.cpp:12-49): tile geometry,
+// redundant recompute and code balance of one variant on a grid, and the rooflines they imply.
+// Resident CTAs per SM come from shared memory (1 KB reserved per CTA) and threads (registers
+// need the device); SM count from the device when there is one, else 148 (B200).
+struct VariantModel {
+    TileGeom tg;
+    int per_sm = 1, sms = 148;
+    double redundancy = 1, cb_no_l2 = 0, hbm_mlups = 0, fp64_mlups = 0;
+    double noL2_mlups = 0;  // min(HBM / cb_no_l2, FP64 roof): the pruning score of the tuner
+};
+VariantModel model_variant(const Handle& h, const Variant* var, int nz, double hbm_gbs,
+                           double fp64_ops) {
+    VariantModel m;
+    const KindInfo& ki = kKinds[h.kind];
+    const int tb = var->tb;
+    m.per_sm = std::max(1, std::min(233472 / (var->smem_bytes + 1024), 2048 / var->threads));
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+            m.sms = n;
+    }
+    cudaGetLastError();
+    m.tg = tile_geom(h, tb, var, nz, m.sms * m.per_sm);
+    const TileGeom& tg = m.tg;
+    const double useful = double(h.nx) * h.ny * nz;
+    m.redundancy = double(tg.computed_lups) / (useful * tb);
+    // no L2 reuse: every unit streams its CTAs' whole level-0 and aux boxes over its z range
+    // (chunk + 2H planes) from HBM and writes its output tile once
+    const int H = tb * h.R;
+    const int naux = h.kind == K_CONST7 ? 0 : h.kind == K_CONST25 ? 2 : ki.ncoeff;
+    const double per_unit =
+        8.0 * (double(var->cy) * (double(var->lx) * var->ly * (tg.zc_len + 2 * H) +
+                                  double(naux) * var->aux_x * var->aux_y * (tg.zc_len + 2 * H - 2 * h.R)) +
+               double(tg.ox) * tg.oy * tg.zc_len);
+    m.cb_no_l2 = per_unit * tg.units / (useful * tb);
+    const double hbm = (hbm_gbs > 0 ? hbm_gbs : 6548.8) * 1e9;  // MEASURED_PEAKS.json fallback
+    const double fp = fp64_ops > 0 ? fp64_ops : 18.59e12;        // measured DMUL+DADD rate
+    m.hbm_mlups = hbm * tb / ki.b1 / 1e6;
+    m.fp64_mlups = fp / (ki.dp_ops * m.redundancy) / 1e6;
+    m.noL2_mlups = std::min(hbm / m.cb_no_l2 / 1e6, m.fp64_mlups);
+    return m;
+}
+}  // namespace
 
 int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double* best_mlups,
                    int* n_measured) {
@@ -3043,17 +2943,37 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
             }
         const girih_gpu_config cfg_saved = h.cfg;
         int measured = 0;
-        // candidates: compiled variants of this kind with tb <= cap, times z-chunk choices
+        // candidates: every compiled variant of this kind with tb <= cap -- fused depth, tile,
+        // prefetch depths, y clusters and output path are independent axes of that table --
+        // pruned by the capacity / code-balance model before anything is measured (the
+        // counterpart of prune_keep, tuner.cpp:41-45): keep those whose no-L2-reuse roof
+        // min(HBM / modelled bytes per LUP, FP64 roof) is within half of the best, and order
+        // them by it so the variant axis of the hill-climb walks from better to worse models
         int nv;
         const Variant* vt = variant_table(h.kind, &nv);
-        std::vector<int> vars;
+        const int nzl = h.slabs[0].zout_hi - h.slabs[0].zout_lo;
+        std::vector<std::pair<double, int>> scored;
         for (int i = 0; i < nv; ++i)
-            if (vt[i].tb <= tb_cap) vars.push_back(global_index_of(&vt[i]));
+            if (vt[i].tb <= tb_cap)
+                scored.push_back({model_variant(h, &vt[i], nzl, 0, 0).noL2_mlups,
+                                  global_index_of(&vt[i])});
+        const double top = std::max_element(scored.begin(), scored.end())->first;
+        std::stable_sort(scored.begin(), scored.end(),
+                         [](const auto& x, const auto& y) { return x.first > y.first; });
+        // start at the configuration the handle would run by default, so the search can only
+        // move to a measured improvement over it
+        const int def_tb = cfg_saved.tb > 0 ? cfg_saved.tb : default_tb_for(h);
+        const int def_var = global_index_of(select_variant(h.kind, std::min(def_tb, tb_cap),
+                                                           def_tb <= tb_cap ? cfg_saved.variant : -1));
+        std::vector<int> vars;
+        for (auto& sc : scored)
+            if (sc.first >= 0.5 * top || sc.second == def_var) vars.push_back(sc.second);
         const int zopts[] = {0, 1, 2, 4, 8, 16};
         const int nz_opts = int(sizeof(zopts) / sizeof(zopts[0]));
         // scheduling axis, the counterpart of the reference tuning its wavefront variant
         // (FED / relaxed, tuner.cpp:146-210): one launch per pass, or chained passes (the
-        // device TileScheduler); only single-slab handles can chain
+        // device TileScheduler); only single-slab handles with non-cluster tiles
+        // chain
         const int copts[] = {-1, 1};
         const int nc_opts = (h.slabs.size() == 1 && h.nranks == 1) ? 2 : 1;
         std::map<std::array<int, 3>, double> seen;
@@ -3062,6 +2982,7 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
             const std::array<int, 3> key{vi, zi, ci};
             if (auto it = seen.find(key); it != seen.end()) return it->second;
             const Variant* v = variant_by_global(vars[vi]);
+            if (copts[ci] > 0 && v->cy > 1) return 0.0;  // cluster tiles do not chain
             girih_gpu_config c = cfg_saved;
             c.tb = v->tb;
             c.variant = vars[vi];
@@ -3087,9 +3008,9 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
             return last;
         };
         // hill_climb (tuner.cpp:73-104): axis-aligned, strict improvement, memoised
-        int bv = 0, bz = 0, bc = 0;
-        for (size_t i = 0; i < vars.size(); ++i)  // start at the largest fused depth
-            if (variant_by_global(vars[i])->tb >= variant_by_global(vars[bv])->tb) bv = int(i);
+        int bv = int(std::find(vars.begin(), vars.end(), def_var) - vars.begin());
+        int bz = 0;
+        int bc = 0;  // one launch per pass (the auto policy's large-grid choice)
         double bs = measure(bv, bz, bc);
         while (true) {
             int nv2 = bv, nz2 = bz, nc2 = bc;
@@ -3146,12 +3067,8 @@ int girih_gpu_model(int kind, int nx, int ny, int nz, int tb, int variant, doubl
         h.cfg.tb = tb;
         const Variant* var = select_variant(kind, tb, variant);
         if (var->tb != tb) throw_err(GIRIH_EINVAL, "variant does not match the fused depth");
-        // resident CTAs per SM from shared memory (1 KB reserved per CTA) and threads; the
-        // register bound needs the device and is left to the occupancy query at run time
-        const int per_sm = std::max(1, std::min(233472 / (var->smem_bytes + 1024), 2048 / var->threads));
-        const int sms = 148;
-        const TileGeom tg = tile_geom(h, tb, var, nz, sms * per_sm);
-        const double useful = double(nx) * ny * nz;
+        const VariantModel vm = model_variant(h, var, nz, hbm_gbs, fp64_ops);
+        const TileGeom& tg = vm.tg;
         std::memset(out, 0, sizeof *out);
         out->tb = tb;
         out->variant = global_index_of(var);
@@ -3161,25 +3078,16 @@ int girih_gpu_model(int kind, int nx, int ny, int nz, int tb, int variant, doubl
         out->oy = tg.oy;
         out->threads = var->threads;
         out->smem_bytes = var->smem_bytes;
-        out->ctas_per_sm = per_sm;
+        out->ctas_per_sm = vm.per_sm;
         out->tiles_x = tg.tiles_x;
         out->tiles_y = tg.tiles_y;
         out->zchunks = tg.nzc;
         out->zc_len = tg.zc_len;
-        out->redundancy = double(tg.computed_lups) / (useful * tb);
+        out->redundancy = vm.redundancy;
         out->code_balance = double(ki.b1) / tb;
-        // no L2 reuse: every unit streams its whole level-0 box and aux box over its z range
-        // (chunk + 2H planes) from HBM and writes its output tile once
-        const int H = tb * h.R;
-        const int naux = kind == K_CONST7 ? 0 : kind == K_CONST25 ? 2 : ki.ncoeff;
-        const double per_unit = 8.0 * (double(var->lx) * var->ly * (tg.zc_len + 2 * H) +
-                                       double(naux) * var->aux_x * var->aux_y * (tg.zc_len + 2 * H - 2 * h.R) +
-                                       double(tg.ox) * tg.oy * tg.zc_len);
-        out->code_balance_no_l2 = per_unit * tg.units / (useful * tb);
-        const double hbm = (hbm_gbs > 0 ? hbm_gbs : 6558.7) * 1e9;
-        const double fp = fp64_ops > 0 ? fp64_ops : 18.59e12;
-        out->hbm_mlups = hbm * tb / ki.b1 / 1e6;
-        out->fp64_mlups = fp / (ki.dp_ops * out->redundancy) / 1e6;
+        out->code_balance_no_l2 = vm.cb_no_l2;
+        out->hbm_mlups = vm.hbm_mlups;
+        out->fp64_mlups = vm.fp64_mlups;
         out->roofline_mlups = std::min(out->hbm_mlups, out->fp64_mlups);
     });
 }

@@ -335,6 +335,26 @@ def test_tuner_restores_state(girih, oracle):
     assert_state_equal(out, ref, "tuned run")
 
 
+@pytest.mark.parametrize("kind", [0, 1], ids=["const7pt", "var7pt"])
+def test_tuner_at_least_default(girih, kind):
+    # the tuner starts from the default configuration and moves only on a measured strict
+    # improvement, so its choice runs at least as fast as the default (256^3; 5% timing noise)
+    g = girih
+    n, T = 256, 24
+
+    def rate(ds):
+        ds.step(T)
+        return max(ds.step(T).mlups for _ in range(3))
+
+    with g.DeviceState.seeded(kind, g.GridSpec(n, n, n), 42, remap=True) as ds:
+        default = rate(ds)
+        cfg, mlups, nmeas = ds.tune()
+        assert nmeas >= 2
+        ds.set_config(cfg)
+        tuned = rate(ds)
+    assert tuned >= 0.95 * default, (cfg, tuned, default)
+
+
 @pytest.mark.slow
 def test_config1_full_size_bitwise(girih, oracle):
     # BASELINE config 1 (const7pt 256^3, T=100) against the oracle at full size
