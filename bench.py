@@ -435,7 +435,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="girih", choices=["girih", "reference"])
     ap.add_argument("--stencil", default="var7pt", choices=KINDS)
-    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=1024,
+                    help="interior extent (cubic grid); use --size under torchrun (--n is an "
+                         "ambiguous prefix of its own options)")
     ap.add_argument("--nt", type=int, default=200)
     ap.add_argument("--tb", type=int, default=0)
     ap.add_argument("--variant", type=int, default=-1)

@@ -810,6 +810,82 @@ int host_copy_threads() {
     return n;
 }
 
+// A persistent pool of host copy threads (thread creation per copy cost ~0.3 ms per call: 50 ms
+// of a 512^3 drop-in call's 150 chunk copies)
+class HostPool {
+public:
+    explicit HostPool(int n) {
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    int size() const { return int(workers_.size()); }
+    // runs fn(0..n-1) on the pool and the calling thread; returns when all are done
+    void run(int n, const std::function<void(int)>& fn) {
+        std::unique_lock<std::mutex> call(call_mu_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            njobs_ = n;
+            next_ = 0;
+            pending_ = n;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void work() {
+        while (true) {
+            int j;
+            const std::function<void(int)>* f;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!fn_ || next_ >= njobs_) return;
+                j = next_++;
+                f = fn_;
+            }
+            (*f)(j);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    void loop(int) {
+        unsigned seen = 0;
+        while (true) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int njobs_ = 0, next_ = 0, pending_ = 0;
+    unsigned gen_ = 0;
+    bool stop_ = false;
+};
+
+HostPool& host_pool() {
+    static HostPool* pool = new HostPool(host_copy_threads() - 1);  // + the calling thread
+    return *pool;
+}
+
 // memcpy split over the host copy threads (pieces >= 4 MB)
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     const int nt = int(std::min<size_t>(host_copy_threads(), std::max<size_t>(1, bytes >> 22)));
@@ -818,14 +894,12 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
         return;
     }
     const size_t piece = (bytes + nt - 1) / nt;
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) {
-        const size_t a = size_t(t) * piece, n = std::min(piece, bytes - std::min(bytes, a));
-        if (n) th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a,
-                                                 static_cast<const char*>(src) + a, n); });
-    }
-    std::memcpy(dst, src, std::min(piece, bytes));
-    for (auto& t : th) t.join();
+    host_pool().run(nt, [&](int t) {
+        const size_t a = size_t(t) * piece;
+        if (a < bytes)
+            std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a,
+                        std::min(piece, bytes - a));
+    });
 }
 
 // page-locked bounce blocks (grow-only, process-wide; used under pinned_scratch_mutex())

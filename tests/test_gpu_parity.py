@@ -636,7 +636,7 @@ def test_bench_multirank_path_functional(girih):
     env = dict(os.environ, GIRIH_BENCH_SHARED_GPU="1", MASTER_ADDR="127.0.0.1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29631", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--n", "256", "--nt", "20"]
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--size", "256", "--nt", "20"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
