@@ -176,6 +176,22 @@ const Variant* select_chain_variant(int kind, int tb, int requested) {
     return v;
 }
 
+// Default tile of a fused depth on a grid: the table's first entry, except var7pt TB = 2 on
+// planes of >= 768^2 cells, where the direct-output tile with a 2-plane coefficient prefetch is
+// faster (1024^3, same box: 136,200-137,400 vs 128,600-133,600 MLUP/s over z chunkings; at 512^3
+// it is 3.5% slower, profiles/r2_zc1024.jsonl, r2_sweep_dout.jsonl)
+const Variant* default_variant(int kind, int tb, long long plane_cells) {
+    if (kind == K_VAR7 && tb == 2 && plane_cells >= 768LL * 768) {
+        int n;
+        const Variant* t = variant_table(kind, &n);
+        for (int i = 0; i < n; ++i)
+            if (t[i].tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].direct_out &&
+                t[i].aux_prefetch == 2 && t[i].cy == 1)
+                return &t[i];
+    }
+    return select_variant(kind, tb, -1);
+}
+
 inline int parity_of(long long t) { return int(((t % 2) + 2) % 2); }
 
 // ------------------------------------------------------------------------------------------
@@ -1454,6 +1470,15 @@ void order_slabs(Handle& h) {
     }
 }
 
+// the variant of a pass: the configured one when it has this depth, else the grid's default
+const Variant* pass_variant(const Handle& h, int tb) {
+    if ((h.cfg.tb == tb || h.cfg.tb == 0) && h.cfg.variant >= 0) {
+        const Variant* v = select_variant(h.kind, tb, h.cfg.variant);
+        if (v->tb == tb) return v;
+    }
+    return default_variant(h.kind, tb, (long long)h.nx * h.ny);
+}
+
 StepStats do_step(Handle& h, long long steps, bool time_passes) {
     StepStats st;
     if (steps == 0) return st;
@@ -1556,9 +1581,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     }
     for (size_t pidx = 0; pidx < plan.size(); ++pidx) {
         const Pass& ps = plan[pidx];
-        const Variant* var =
-            select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
-        if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+        const Variant* var = pass_variant(h, ps.tb);
         st.variant = global_index_of(var);
         st.tb_used = std::max(st.tb_used, ps.tb);
         const Variant* cvar =
@@ -2077,8 +2100,8 @@ void stream_run(Handle& h, const girih_state_view& v, long long steps, girih_gpu
     //      window's results downloaded right after its last pass; every awaited event is
     //      recorded before it is waited on ----
     const Variant* var2 =
-        single ? nullptr : select_variant(h.kind, 2, h.cfg.tb == 2 ? h.cfg.variant : -1);
-    const Variant* var1 = select_variant(h.kind, 1, h.cfg.tb == 1 ? h.cfg.variant : -1);
+        single ? nullptr : pass_variant(h, 2);
+    const Variant* var1 = pass_variant(h, 1);
     long long computed = 0, units = 0;
     int launches = 0;
     // final level of parity b (single-step mode: the parity-b field itself)
@@ -2863,8 +2886,7 @@ int girih_gpu_update_units(void* handle, long long steps, long long unit_begin,
             for (const Pass& ps : ur.plan) {
                 for (int b : {ps.src, ps.src_prev, ps.dst, ps.dst_penult})
                     if (b >= 2) ensure_scratch(h, b & 1);
-                const Variant* var = select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
-                if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+                const Variant* var = pass_variant(h, ps.tb);
                 LaunchInfo li;
                 const PassParams p = build_params(h, ps, var, 0, t, &li);
                 ur.base.push_back(base);
@@ -2892,8 +2914,7 @@ int girih_gpu_update_units(void* handle, long long steps, long long unit_begin,
                 for (long long u = 0; u < ur.base[q]; ++u)
                     if (!ur.done[size_t(u)])
                         throw_err(GIRIH_ESTATE, "units of an earlier pass are not complete");
-                const Variant* var = select_variant(h.kind, ps.tb, (h.cfg.tb == ps.tb || h.cfg.tb == 0) ? h.cfg.variant : -1);
-                if (var->tb != ps.tb) var = select_variant(h.kind, ps.tb, -1);
+                const Variant* var = pass_variant(h, ps.tb);
                 LaunchInfo li;
                 PassParams p = build_params(h, ps, var, 0, t, &li);
                 p.unit0 = int(a - ur.base[q]);
@@ -3037,8 +3058,8 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         // start at the configuration the handle would run by default, so the search can only
         // move to a measured improvement over it
         const int def_tb = cfg_saved.tb > 0 ? cfg_saved.tb : default_tb_for(h);
-        const int def_var = global_index_of(select_variant(h.kind, std::min(def_tb, tb_cap),
-                                                           def_tb <= tb_cap ? cfg_saved.variant : -1));
+        const int def_var = global_index_of(def_tb <= tb_cap ? pass_variant(h, def_tb)
+                                                             : select_variant(h.kind, tb_cap, -1));
         std::vector<int> vars;
         for (auto& sc : scored)
             if (sc.first >= 0.5 * top || sc.second == def_var) vars.push_back(sc.second);
