@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GIRIH_GPU_ABI_VERSION 3
+#define GIRIH_GPU_ABI_VERSION 4
 
 #define GIRIH_OK 0
 #define GIRIH_EINVAL (-1)
@@ -102,9 +102,11 @@ typedef struct {
     int smem_bytes;
     int cluster_y;          /* CTAs per thread-block cluster along y (1 = none): the cluster's
                                CTAs share the fused levels' halo rows through distributed
-                               shared memory */
+                               shared memory, or (paced = 1) only run in lockstep */
     int aux_prefetch;       /* coefficient planes fetched ahead */
     int direct_out;         /* 1: output stored from registers (no smem staging + TMA store) */
+    int paced;              /* 1: cluster of independent y-neighbour tiles kept on the same z
+                               plane by a per-plane cluster barrier (shared rows hit L2) */
 } girih_gpu_variant;
 
 const char* girih_gpu_last_error(void);

@@ -687,6 +687,8 @@ void setup_geometry(Handle& h, int kind, int nx, int ny, int nz, int pad_x) {
     // 128-byte-aligned one (off = 15); off = 3, 7, 11 are equal. For R = 4 the 128-byte-aligned
     // start (off = 12) is as good as any.
     h.off = R == 1 ? 3 : (16 - R % 16) % 16;
+    if (const char* e = std::getenv("GIRIH_OFF"))  // A/B only (must keep off + R even)
+        if ((std::atoi(e) + R) % 2 == 0 && std::atoi(e) >= 0) h.off = std::atoi(e);
     h.pitch = (h.X + h.off + 15) / 16 * 16;
 }
 
@@ -1204,7 +1206,9 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     t.ox = var->lx - 2 * t.hx;
     // y: one tile = one CTA, or one cluster of cy CTAs whose boxes overlap by 2R rows and
     // share the fused levels' halo rows (zwave.cuh ZwaveConfig::OYC)
-    t.oy = var->cy > 1 ? var->cy * (var->ly - 2 * R) - 2 * (tb - 1) * R : var->ly - 2 * H;
+    t.oy = var->cy == 1 ? var->ly - 2 * H
+           : var->pace  ? var->cy * (var->ly - 2 * H)
+                        : var->cy * (var->ly - 2 * R) - 2 * (tb - 1) * R;
     t.tiles_x = (h.nx + t.ox - 1) / t.ox;
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
@@ -1226,6 +1230,21 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
         t.computed_lups += ex * ey * (long long)txy * ez;
     }
     return t;
+}
+
+// Lockstep pacing of single-pass launches (PassParams::lock) and the group-major unit order
+// that goes with it. GIRIH_LOCK_B = iterations per block (0 = off), GIRIH_LOCK_S = slack in
+// blocks, GIRIH_UGROUP = 0 keeps the z-chunk-major order (A/B switches).
+struct LockCfg {
+    int blk, slack, group, strip;
+};
+LockCfg lock_cfg() {
+    auto env = [](const char* n, int d) {
+        const char* e = std::getenv(n);
+        return e ? std::atoi(e) : d;
+    };
+    return LockCfg{std::max(0, env("GIRIH_LOCK_B", 0)), std::max(1, env("GIRIH_LOCK_S", 2)),
+                   env("GIRIH_UGROUP", 1) != 0 ? 1 : 0, std::max(0, env("GIRIH_USTRIP", 0))};
 }
 
 // Builds the parameters of one pass on one slab (tile grid, z chunks, persistent grid size).
@@ -1335,7 +1354,7 @@ PassDesc single_desc(Handle& h, int slab, const Variant* var, int tb, const Pass
     d.vmap = vmap;
     d.umap = umap;
     const int R = h.R, H = tb * R;
-    if (var->cy > 1) {
+    if (var->cy > 1 && !var->pace) {
         d.omap = tensor_map(h, slab, p.dst_final, 1, p.ox, var->ly - R - H, 1);
         d.omap_in = tensor_map(h, slab, p.dst_final, 1, p.ox, var->ly - 2 * R, 1);
     } else {
@@ -1575,9 +1594,13 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
     // atomicAdd - work_base (the sum of the earlier passes' unit counts; every pass performs
     // exactly `units` increments), so no memset node separates consecutive passes
     std::vector<long long> work_base(h.slabs.size(), 0);
+    // lockstep pacing counter (bytes 8..15 of the work block), cumulative over the step's passes
+    std::vector<unsigned long long> lock_base(h.slabs.size(), 0);
+    const LockCfg lk = lock_cfg();
     for (Slab& s : h.slabs) {
         GCHECK(cudaSetDevice(s.device));
         GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
+        GCHECK(cudaMemsetAsync(reinterpret_cast<char*>(s.work->p) + 8, 0, 8, s.stream));
     }
     for (size_t pidx = 0; pidx < plan.size(); ++pidx) {
         const Pass& ps = plan[pidx];
@@ -1679,6 +1702,19 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             }
             p.work_base = int(work_base[g]);
             work_base[g] += p.units;
+            if (lk.strip > 0 && !h.instr.on) p.ustrip = lk.strip;
+            if (lk.blk > 0 && var->cy == 1 && !h.instr.on && p.units > li.grid) {
+                if (lock_base[g] > (1ull << 62)) {
+                    GCHECK(cudaMemsetAsync(reinterpret_cast<char*>(s.work->p) + 8, 0, 8, s.stream));
+                    lock_base[g] = 0;
+                }
+                p.lock = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(s.work->p) + 8);
+                p.lock_base = lock_base[g];
+                p.lock_blk = lk.blk;
+                p.lock_slack = lk.slack;
+                lock_base[g] += (unsigned long long)li.grid << 32;  // 2^32 arrivals per CTA
+                if (lk.group) p.ugroup = li.grid;
+            }
             const CUtensorMap& vmap = tensor_map(h, int(g), s.buf[ps.src]->p, 1, var->lx, var->ly);
             const CUtensorMap* cmap = &vmap;
             const CUtensorMap* umap = &vmap;
@@ -2391,6 +2427,7 @@ int girih_gpu_variant_info(int index, girih_gpu_variant* out) {
         out->cluster_y = v->cy;
         out->aux_prefetch = v->aux_prefetch;
         out->direct_out = v->direct_out;
+        out->paced = v->pace;
     });
 }
 

@@ -25,6 +25,7 @@ struct Variant {
     OccFn occupancy;             // resident CTAs, single-pass kernel (a multiple of cy)
     OccFn occupancy_chain;       // the same for the chained kernel
     int direct_out;              // 1: output level stored straight from registers (no staging)
+    int pace;                    // 1: the cluster only paces independent tiles (no shared rows)
 };
 
 // one table per kind, defined in variants_<kind>.cu
@@ -155,7 +156,7 @@ cudaError_t occupancy_zwave(int* max_ctas) {
             &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                       \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                          \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF, true>,                    \
-            ((CF) >> 8) & 1                                                                   \
+            ((CF) >> 8) & 1, ((CF) >> 9) & 1                                                  \
     }
 // CY CTAs per y cluster
 #define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \
@@ -163,6 +164,9 @@ cudaError_t occupancy_zwave(int* max_ctas) {
 // direct output stores (no staging planes)
 #define GIRIH_VARIANT_D(KIND, TB, LX, LY, NT, P, PA, MINB) \
     GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, 1 | (1 << 8))
+// clusters of CY y-neighbour tiles paced in lockstep (ZwaveConfig::PACE), direct output
+#define GIRIH_VARIANT_PD(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \
+    GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, (CY) | (1 << 8) | (1 << 9))
 #define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB) \
     GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, 1)
 

@@ -56,6 +56,9 @@
 #ifndef GIRIH_ZPS
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
 #endif
+#ifndef GIRIH_LOCK
+#define GIRIH_LOCK 1  // lockstep pacing code compiled in (PassParams::lock)
+#endif
 #ifndef GIRIH_XSHFL
 #define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
 #endif
@@ -118,6 +121,26 @@ struct PassParams {
     int trace_pass;
     unsigned* ledger;
     int ledger_t;  // step index (from the start of the call) of this pass's level 1
+    // Lockstep (single-pass, non-cluster launches; off when lock is null). The CTAs of a
+    // persistent grid drift apart under dynamic unit drawing until neighbouring tiles stream
+    // the same planes tens of iterations apart, beyond the ~13 iterations a plane stays in L2,
+    // and every shared halo row then comes from DRAM twice. Each CTA's load producer counts its
+    // issued planes in blocks of lock_blk and may not start block m before every CTA of the
+    // grid has reached block m - lock_slack: *lock counts block arrivals from lock_base on
+    // (relaxed atomics: pure pacing, no data is exchanged). A CTA out of units adds the
+    // remainder of its 2^32 arrivals, so the rest never wait for it. Every CTA of the grid is
+    // resident (grid <= occupancy x SMs), so the slowest CTA never waits.
+    unsigned long long* lock;
+    unsigned long long lock_base;
+    int lock_blk, lock_slack;
+    // unit order: 0 = z-chunk-major; G > 0 = groups of G tiles (the grid size), z chunk inside
+    // the group, so a tile's next z chunk is drawn one wave after its previous one and
+    // re-reads that chunk's last 2H planes from L2 (with lockstep) instead of DRAM
+    int ugroup;
+    // tile order inside a z-chunk row: 0 = row-major (x fastest); W > 0 = column strips of W
+    // tiles, y fastest inside a strip, so y-neighbour tiles are W draws apart instead of a whole
+    // tile row (units drawn close together start close together and share L2 halo rows)
+    int ustrip;
 };
 
 // Pass chaining. One launch may run a sequence of passes over the same tile grid. Units are
@@ -277,10 +300,29 @@ struct UnitGeom {
 
 __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
     UnitGeom g;
-    g.tx = u % p.tiles_x;
-    const int r = u / p.tiles_x;
-    g.ty = r % p.tiles_y;
-    const int zc = r / p.tiles_y;
+    int zc;
+    if (p.ugroup > 0) {  // groups of ugroup tiles, z chunk inside the group (the last is short)
+        const int txy = p.tiles_x * p.tiles_y, per = p.ugroup * p.nzc;
+        const int grp = u / per, w = u - grp * per;
+        const int gsz = min(p.ugroup, txy - grp * p.ugroup);
+        zc = w / gsz;
+        const int tile = grp * p.ugroup + (w - zc * gsz);
+        g.tx = tile % p.tiles_x;
+        g.ty = tile / p.tiles_x;
+    } else if (p.ustrip > 0) {
+        const int txy = p.tiles_x * p.tiles_y;
+        zc = u / txy;
+        const int tile = u - zc * txy, sw = p.ustrip * p.tiles_y;  // tiles per full strip
+        const int strip = tile / sw, w = min(p.ustrip, p.tiles_x - strip * p.ustrip);
+        const int r = tile - strip * sw;
+        g.ty = r / w;
+        g.tx = strip * p.ustrip + (r - g.ty * w);
+    } else {
+        g.tx = u % p.tiles_x;
+        const int r = u / p.tiles_x;
+        g.ty = r % p.tiles_y;
+        zc = r / p.tiles_y;
+    }
     g.za = p.zout_lo + zc * p.zc_len;
     g.zb = min(g.za + p.zc_len, p.zout_hi);
     return g;
@@ -434,10 +476,18 @@ struct ZwaveConfig {
     // of level s-1 beyond an INNER edge are the neighbour's own rows, which it pushes into this
     // CTA's ring through distributed shared memory. Only the cluster's outer edges keep the
     // trapezoid halo, so the redundant rows per CTA drop from 2(TB-1)R to 2(TB-1)R/CY.
-    static constexpr int OWN = LY - 2 * R;
-    static constexpr int OYS = CY > 1 ? OWN : OY;                 // widest output rows of a CTA
-    static constexpr int OYC = CY > 1 ? CY * OWN - 2 * (TB - 1) * R : OY;  // per cluster
-    static constexpr int OYE = CY > 1 ? LY - R - H : OY;          // outer CTAs' output rows
+    // PACE (flag 2): the cluster only paces its CTAs. Each CTA computes an ordinary trapezoid
+    // tile (OY output rows, the box of CTA c starts c*OY rows above CTA c-1's) and nothing is
+    // exchanged; the per-iteration cluster barrier keeps the CY y-neighbours on the same z
+    // plane, so the level-0 and coefficient rows their boxes share are read from DRAM once and
+    // hit L2 for the second reader (free-running CTAs drift apart by more than a plane's L2
+    // lifetime).
+    static constexpr bool PACE = ((CF >> 9) & 1) != 0;
+    static constexpr bool SHARE = CY > 1 && !PACE;                // DSMEM-shared halo rows
+    static constexpr int OWN = PACE ? OY : LY - 2 * R;
+    static constexpr int OYS = SHARE ? OWN : OY;                  // widest output rows of a CTA
+    static constexpr int OYC = CY > 1 ? (PACE ? CY * OY : CY * OWN - 2 * (TB - 1) * R) : OY;
+    static constexpr int OYE = SHARE ? LY - R - H : OY;           // outer CTAs' output rows
     static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
     // threads cover the level-1 valid rows [R, LY - R) only: the R outermost rows of the
@@ -476,7 +526,7 @@ struct ZwaveConfig {
     static_assert((LX * 8) % 16 == 0 && (AX * 8) % 16 == 0, "TMA inner box must be 16-byte multiple");
     static_assert((CELLS * 8) % 128 == 0 && (AYX * 8) % 128 == 0, "TMA smem boxes 128-byte aligned");
     static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
-    static_assert(CY == 1 || (TB >= 2 && OYE > 0 && OWN >= 2 * R && CY <= 16),
+    static_assert(CY == 1 || PACE || (TB >= 2 && OYE > 0 && OWN >= 2 * R && CY <= 16),
                   "clusters share fused-level halo rows: TB >= 2, outer CTAs need output rows");
 };
 
@@ -523,7 +573,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     // cluster position (CY > 1): rank c owns box rows [R, LY-R) of the cluster tile's c-th box;
     // the outer CTAs (c = 0, CY-1) keep the trapezoid halo on their outer side
     const int crank = CY > 1 ? int(cluster_ctarank()) : 0;
-    const bool lo_edge = crank == 0, hi_edge = crank == CY - 1;
+    // (PACE: every CTA is a whole trapezoid tile, both edges outer)
+    const bool lo_edge = CFG::PACE || crank == 0, hi_edge = CFG::PACE || crank == CY - 1;
     const int oy_lo = lo_edge ? H : R;  // first output row of this CTA's box
     if (tid == 0) {
         for (int b = 0; b < NR0; ++b) mbar_init(&vbar[b], 1);
@@ -539,13 +590,46 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     Cursor vcur{}, acur{};
     uint32_t vnext = G0, anext = G0;
     int drawn = 0;  // producer: next unit id, drawn one unit ahead
+    bool lock_done = false;  // lockstep: this CTA has released the others
     // chained launches: the V cursor's unit passed its dependency check; the store thread's
     // finished unit whose last plane is the pending store
     bool vready = false;
     int pub_next = -1;
     // returns false when a chained unit's dependencies are not met yet and `must` is false
     auto issue_v = [&](bool must) -> bool {
-        if (vcur.u >= total) return false;
+        if (vcur.u >= total) {
+            if constexpr (!CHAIN && CY == 1 && GIRIH_LOCK) {
+                if (p.lock && !lock_done) {  // out of units: release the others for good
+                    const unsigned arrived = (vnext - G0 + unsigned(p.lock_blk) - 1) / unsigned(p.lock_blk);
+                    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p.lock),
+                                 "l"((1ull << 32) - arrived)
+                                 : "memory");
+                    lock_done = true;
+                }
+            }
+            return false;
+        }
+        if constexpr (!CHAIN && CY == 1 && GIRIH_LOCK) {
+            if (p.lock && (vnext - G0) % unsigned(p.lock_blk) == 0) {
+                const unsigned m = (vnext - G0) / unsigned(p.lock_blk);  // block of this plane
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p.lock) : "memory");
+                if (m >= unsigned(p.lock_slack)) {
+                    const unsigned long long need =
+                        p.lock_base + (unsigned long long)(m - p.lock_slack + 1) * gridDim.x;
+                    long long spins = 0;
+                    for (;;) {
+                        unsigned long long a;
+                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(p.lock));
+                        if (a >= need) break;
+                        __nanosleep(32);
+                        if (++spins > (1ll << 28)) {  // watchdog: flag for the host, proceed
+                            atomicExch(p.work + 1, 1);
+                            break;
+                        }
+                    }
+                }
+            }
+        }
         if constexpr (CHAIN) {
             if (vcur.it == 0 && vcur.q > 0 && !vready) {
                 const int ul = vcur.u - vcur.q * p.units;
@@ -1165,16 +1249,25 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                             double* pen = has_penult_1
                                               ? (side ? p.push_up_penult : p.push_dn_penult) + o
                                               : nullptr;
+                            // a full pair is one aligned 16-byte store (the neighbour's buffers
+                            // share this layout and the offsets are whole planes), so a warp's
+                            // push is 512 contiguous bytes of NVLink writes, not 32 strided
+                            // 8-byte ones per cell of the pair
 #pragma unroll
                             for (int i = 0; i < PPT; ++i) {
                                 const double2 c2 =
                                     ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : (R + PH) % ZQD];
+                                const uint32_t m = ((out_mask & ~ghost_mask) >> (2 * i)) & 3u;
+                                if (m == 3u) {
+                                    *reinterpret_cast<double2*>(fin + colidx[2 * i]) = val[i];
+                                    if (pen) *reinterpret_cast<double2*>(pen + colidx[2 * i]) = c2;
+                                } else {
 #pragma unroll
-                                for (int q = 0; q < 2; ++q) {
-                                    const int b = 2 * i + q;
-                                    if (!((out_mask >> b) & 1) || ((ghost_mask >> b) & 1)) continue;
-                                    fin[colidx[b]] = q ? val[i].y : val[i].x;
-                                    if (pen) pen[colidx[b]] = q ? c2.y : c2.x;
+                                    for (int q = 0; q < 2; ++q) {
+                                        if (!((m >> q) & 1u)) continue;
+                                        fin[colidx[2 * i + q]] = q ? val[i].y : val[i].x;
+                                        if (pen) pen[colidx[2 * i + q]] = q ? c2.y : c2.x;
+                                    }
                                 }
                             }
                         }

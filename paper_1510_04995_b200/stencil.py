@@ -154,7 +154,8 @@ def variants():
         check(lib.girih_gpu_variant_info(i, C.byref(v)))
         out.append(dict(index=i, kind=v.kind, tb=v.tb, lx=v.lx, ly=v.ly, threads=v.threads,
                         prefetch=v.prefetch, smem_bytes=v.smem_bytes, cluster_y=v.cluster_y,
-                        aux_prefetch=v.aux_prefetch, direct_out=v.direct_out))
+                        aux_prefetch=v.aux_prefetch, direct_out=v.direct_out,
+                        paced=v.paced))
     return out
 
 

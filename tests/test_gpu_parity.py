@@ -289,6 +289,33 @@ def test_device_state_stepwise_equals_single_run(girih, oracle):
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_lockstep_pacing_and_group_order(girih, oracle, kind, monkeypatch):
+    # single-pass launches with more units than resident CTAs pace their CTAs in lockstep
+    # (PassParams::lock) and draw units in tile groups of the grid size with the z chunk inside
+    # the group (PassParams::ugroup): pure scheduling, results must not change. Forced z chunks
+    # give more units than the persistent grid holds; several block/slack settings, tight to
+    # loose, and the chained path disabled so every pass is a single launch.
+    g = girih
+    hs = oracle.init_state(kind, 150, 130, 90, 1, 12, remap=True)
+    tb = max(v["tb"] for v in g.variants() if v["kind"] == kind and v["cluster_y"] == 1)
+    steps = 2 * tb + 1
+    ref = hs.copy()
+    oracle.naive_sweep(ref, steps)
+    for blk, slack, group, strip in ((4, 2, 1, 0), (1, 1, 1, 0), (3, 1, 0, 2), (0, 1, 1, 0),
+                                     (0, 1, 1, 2), (0, 1, 1, 3)):
+        monkeypatch.setenv("GIRIH_LOCK_B", str(blk))
+        monkeypatch.setenv("GIRIH_LOCK_S", str(slack))
+        monkeypatch.setenv("GIRIH_UGROUP", str(group))
+        monkeypatch.setenv("GIRIH_USTRIP", str(strip))
+        with g.DeviceState.from_state(to_problem(g, hs),
+                                      g.GpuConfig(tb=tb, zchunks=30, chain=-1)) as ds:
+            rep = ds.step(steps)
+            assert rep.units > rep.grid_ctas * rep.n_launches, "needs more units than CTAs"
+            out = ds.download()
+        assert_state_equal(out, ref, f"lock blk={blk} slack={slack} group={group} strip={strip}")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_emulated_z_slabs_bitwise(girih, oracle, kind):
     # the multi-GPU z-slab decomposition (halo depth R*TBmax, exchange after every pass) run as
     # several slabs on one device: must equal the single-domain oracle bitwise

@@ -36,6 +36,21 @@ namespace {
 
 constexpr int kSchemaVersion = 1;
 
+// measured HBM copy bandwidth: --hbm, else "hbm_gbs" of MEASURED_PEAKS.json (driver-written; in
+// $GIRIH_PEAKS or the working directory), else 0 = the library's own fallback
+double measured_hbm_gbs(double flag) {
+    if (flag > 0) return flag;
+    const char* env = std::getenv("GIRIH_PEAKS");
+    std::ifstream in(env ? env : "MEASURED_PEAKS.json");
+    std::stringstream ss;
+    ss << in.rdbuf();
+    const std::string s = ss.str();
+    const size_t k = s.find("\"hbm_gbs\"");
+    if (k == std::string::npos) return 0.0;
+    const size_t c = s.find(':', k);
+    return c == std::string::npos ? 0.0 : std::atof(s.c_str() + c + 1);
+}
+
 struct Options {
     std::string cmd;
     std::string stencil = "const7pt";
@@ -271,7 +286,8 @@ int cmd_run(const Options& o) {
     const double mlups = ksec > 0 ? lups / ksec / 1e6 : 0.0;
     const double cb = best.model_bytes_per_lup;
     const double hbm_gbs = mlups * 1e6 * cb / 1e9;
-    const double hbm_peak = 6558.7;  // MEASURED_PEAKS.json hbm_gbs
+    const double hbm_flag = measured_hbm_gbs(o.hbm);
+    const double hbm_peak = hbm_flag > 0 ? hbm_flag : 6548.8;  // fallback: the round-1 pool
     const double roof = cb > 0 ? hbm_peak * 1e9 / cb / 1e6 : 0.0;
     std::ostringstream rec;
     const double glups = (wall > 0 && lups > 0) ? lups / wall / 1e9 : 0.0;
@@ -354,7 +370,7 @@ int cmd_model(const Options& o) {
         for (int tb : tbs) {
             girih_gpu_model_out m{};
             gpu::check(girih_gpu_model(int(kind), o.nx, o.ny, o.nz, tb, o.tb > 0 ? o.variant : -1,
-                                       o.hbm, o.fp64, &m));
+                                       measured_hbm_gbs(o.hbm), o.fp64, &m));
             std::printf("%s,%d,%d,%dx%d,%dx%d,%d,%d,%d,%d,%.4f,%.3f,%.3f,%.0f,%.0f,%.0f,%.3f,%.1f\n",
                         name.c_str(), m.tb, m.variant, m.lx, m.ly, m.ox, m.oy, m.threads,
                         m.smem_bytes, m.ctas_per_sm, m.zchunks, m.redundancy, m.code_balance,
