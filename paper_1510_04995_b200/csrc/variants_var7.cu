@@ -29,8 +29,6 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT_D(K_VAR7, 2, 64, 18, 512, 2, 2, 1),
     GIRIH_VARIANT_D(K_VAR7, 2, 64, 17, 480, 2, 2, 1),
     GIRIH_VARIANT_PD(K_VAR7, 2, 64, 18, 512, 2, 2, 1, 2),
-    GIRIH_VARIANT_PD(K_VAR7, 2, 64, 18, 512, 2, 1, 1, 2),
-    GIRIH_VARIANT_PD(K_VAR7, 2, 64, 18, 512, 2, 2, 1, 4),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

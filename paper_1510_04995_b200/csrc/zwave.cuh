@@ -59,6 +59,9 @@
 #ifndef GIRIH_LOCK
 #define GIRIH_LOCK 1  // lockstep pacing code compiled in (PassParams::lock)
 #endif
+#ifndef GIRIH_PACE_LAG
+#define GIRIH_PACE_LAG 2  // PACE clusters: planes a CTA may run ahead of its y-neighbours
+#endif
 #ifndef GIRIH_XSHFL
 #define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
 #endif
@@ -204,6 +207,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 __device__ __forceinline__ void tma_load_plane(void* dst, const CUtensorMap* map, int x, int y,
                                                int z, uint64_t* bar) {
     asm volatile(
@@ -271,6 +286,11 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void st_cluster_d2(uint32_t addr, double2 v) {
     asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y)
+                 : "memory");
+}
+// arrive on an mbarrier in another CTA of the cluster (pacing: PACE clusters)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
 __device__ __forceinline__ void st_cluster_s32(uint32_t addr, int v) {
@@ -549,6 +569,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     constexpr int OWN = CFG::OWN, OYC = CFG::OYC;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr bool CQ = CFG::CQ;
+    // PACE clusters: no per-plane cluster barrier. Thread 0 of each CTA arrives, per finished
+    // iteration, on its y-neighbours' pace barriers (a ring of PK mbarriers, one per iteration
+    // mod PK) and, before issuing the next loads, waits until the neighbours have finished all
+    // but the last PD iterations it has: the neighbours stay within PD planes of each other
+    // with no stall while they are (a neighbour is never more than PD+1 iterations ahead, so
+    // PK > 2(PD+1) keeps the ring's phases unambiguous).
+    constexpr bool PACE = CFG::PACE;
+    constexpr bool CSYNC = CY > 1 && !PACE && !GIRIH_CLUSTER_NOSYNC;  // per-plane cluster barrier
+    constexpr int PK = 8, PD = GIRIH_PACE_LAG;
+    static_assert(PK > 2 * (PD + 1), "pace ring too short for the lag");
     // x neighbours by warp shuffle (misaligned pair loads cost two shared-memory wavefronts
     // per quarter warp). Measured (same box): const7pt single-pass +4.5% (512^3); const7pt
     // chained -15%, var7pt -2%, const25pt -5% (radius 4: 16 shuffles per pair), var25pt +-0.
@@ -570,6 +600,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     uint64_t* abar = vbar + NR0;
 
     const int tid = threadIdx.x;
+    __shared__ uint64_t pbar[PACE ? PK : 1];
     // cluster position (CY > 1): rank c owns box rows [R, LY-R) of the cluster tile's c-th box;
     // the outer CTAs (c = 0, CY-1) keep the trapezoid halo on their outer side
     const int crank = CY > 1 ? int(cluster_ctarank()) : 0;
@@ -579,11 +610,20 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     if (tid == 0) {
         for (int b = 0; b < NR0; ++b) mbar_init(&vbar[b], 1);
         for (int b = 0; b < NAR; ++b) mbar_init(&abar[b], 1);
+        if constexpr (PACE)  // one arrival per y-neighbour and iteration
+            for (int b = 0; b < PK; ++b)
+                mbar_init(&pbar[b], uint32_t((crank > 0 ? 1 : 0) + (crank < CY - 1 ? 1 : 0)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async_smem();
     }
     __syncthreads();
 
+    // PACE: iteration i finished -> one arrival on each y-neighbour's pace barrier i % PK
+    [[maybe_unused]] auto pace_arrive = [&](uint32_t i) {
+        const uint32_t a = smem_u32(&pbar[PACE ? i % PK : 0]);
+        if (crank > 0) mbar_arrive_remote(mapa_rank(a, uint32_t(crank - 1)));
+        if (crank < CY - 1) mbar_arrive_remote(mapa_rank(a, uint32_t(crank + 1)));
+    };
     // ---- producers (thread 0): V runs P elements ahead, aux PA elements ahead ----
     __shared__ int uq[UQ];
     const int total = CHAIN ? cd.npass * p.units : p.unit_n;  // units of the launch
@@ -726,7 +766,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             for (int e = 0; e < P; ++e) issue_v(true);
             for (int e = 0; e < PA; ++e) issue_a();
         }
-        cluster_arrive();  // pairs with the first iteration's wait
+        if constexpr (!PACE) cluster_arrive();  // pairs with the first iteration's wait
     } else if (tid == 0) {
         // single-pass launches: the first unit is blockIdx.x. Chained launches draw it too, so
         // that every unit another CTA may wait for belongs to a CTA that is already running
@@ -921,6 +961,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     if constexpr (NAUX > 0)
                         while (anext <= g + PA && anext < vnext) issue_a();
                 } else {
+                    if constexpr (PACE) {
+                        const uint32_t m = g - G0;  // iterations this CTA has finished
+                        if (m > 0) pace_arrive(m - 1);
+                        if (m > PD) {
+                            const uint32_t i = m - 1 - PD;  // neighbours must have finished it
+                            // acquire at cluster scope: the leader's remote unit-queue
+                            // stores before its arrivals are visible after this wait
+                            mbar_wait_cluster(&pbar[i % PK], (i / PK) & 1);
+                        }
+                    }
                     issue_v(true);
                     issue_a();
                 }
@@ -982,7 +1032,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             [[maybe_unused]] bool cwaited = false;
 #pragma unroll
             for (int s = 1; s <= TB; ++s) {
-                if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC) {
+                if constexpr (CSYNC) {
                     if (s == 2) {
                         cluster_wait();
                         cwaited = true;
@@ -1275,7 +1325,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     staged = !DOUT;
                 }
             }
-            if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC)
+            if constexpr (CSYNC)
                 if (!cwaited) cluster_wait();
             // deferred centre-ring stores of levels 1..TB-1 (read by other threads from the
             // next iteration on, behind the barrier)
@@ -1300,7 +1350,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     }
                 }
             }
-            if constexpr (CY > 1 && !GIRIH_CLUSTER_NOSYNC)
+            if constexpr (CSYNC)
                 cluster_arrive();  // this iteration's ring rows are complete
             // advance every level's z queue by one plane (and the coefficient queue)
             if constexpr (CQ) {
@@ -1379,7 +1429,15 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             unroll_phases<0, NPH>(phase);
         }
     }
-    if constexpr (CY > 1) cluster_wait();  // no CTA leaves while a neighbour may push into it
+    if constexpr (PACE) {
+        // the last iteration's arrival (a neighbour may still wait for it), then no CTA leaves
+        // while a neighbour may still arrive on its barriers
+        if (tid == 0 && g > G0) pace_arrive(g - G0 - 1);
+        cluster_arrive();
+        cluster_wait();
+    } else if constexpr (CY > 1) {
+        cluster_wait();  // no CTA leaves while a neighbour may push into it
+    }
     __syncthreads();
     if (tid == STORE_TID) {
         if (pend) {
