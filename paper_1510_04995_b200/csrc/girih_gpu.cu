@@ -176,18 +176,23 @@ const Variant* select_chain_variant(int kind, int tb, int requested) {
     return v;
 }
 
-// Default tile of a fused depth on a grid: the table's first entry, except var7pt TB = 2 on
-// planes of >= 768^2 cells, where the direct-output tile with a 2-plane coefficient prefetch is
-// faster (1024^3, same box: 136,200-137,400 vs 128,600-133,600 MLUP/s over z chunkings; at 512^3
-// it is 3.5% slower, profiles/r2_zc1024.jsonl, r2_sweep_dout.jsonl)
+// Default tile of a fused depth on a grid: the table's first entry, except var7pt TB = 2, where
+// the direct-output tile with a 2-plane coefficient prefetch is faster at every size measured
+// (same box, fresh processes, MLUP/s vs the staged 64x18 tile: 256^3 110.7 K vs 101.0 K, 384^3
+// 127.3 K vs 125.6 K, 512^3 136.4 K vs 130.5 K, 768^3 141.2 K vs 132.4 K; 1024^3 136.2-137.4 K vs
+// 128.6-133.6 K; profiles/r2_default_variant_ab.txt)
+// const7pt TB = 1 single-pass launches likewise take the direct-output 64x10 tile (256^3 225 K vs
+// 198 K, 384^3 309 K vs 267 K, 512^3 325 K vs 288 K); chained launches keep the staged tile
+// (select_chain_variant: 256^3 281 K vs 273 K).
 const Variant* default_variant(int kind, int tb, long long plane_cells) {
-    if (kind == K_VAR7 && tb == 2 && plane_cells >= 768LL * 768) {
-        int n;
-        const Variant* t = variant_table(kind, &n);
-        for (int i = 0; i < n; ++i)
-            if (t[i].tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].direct_out &&
-                t[i].aux_prefetch == 2 && t[i].cy == 1)
-                return &t[i];
+    (void)plane_cells;
+    int n;
+    const Variant* t = variant_table(kind, &n);
+    for (int i = 0; i < n; ++i) {
+        if (t[i].tb != tb || !t[i].direct_out || t[i].cy != 1) continue;
+        if (kind == K_VAR7 && tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].aux_prefetch == 2)
+            return &t[i];
+        if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10) return &t[i];
     }
     return select_variant(kind, tb, -1);
 }
@@ -1447,10 +1452,12 @@ void ipc_before_pass(Handle& h) {
         if (r != CUDA_SUCCESS) throw_err(GIRIH_ECUDA, "cuStreamWaitValue32 failed");
     }
 }
-void ipc_after_pass(Handle& h) {
+// kernel_signalled: the pass's last boundary unit already wrote the flags (zwave.cuh bflag_*)
+void ipc_after_pass(Handle& h, bool kernel_signalled = false) {
     static StreamValueFn write = stream_value_fn("cuStreamWriteValue32");
     Slab& s = h.slabs[0];
     ++h.epoch;
+    if (kernel_signalled) return;
     for (int side = 0; side < 2; ++side) {
         if (!h.peer[side].open) continue;
         // our pass count goes into the neighbour's entry for the side we are on
@@ -1601,7 +1608,9 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         GCHECK(cudaSetDevice(s.device));
         GCHECK(cudaMemsetAsync(s.work->p, 0, sizeof(int), s.stream));
         GCHECK(cudaMemsetAsync(reinterpret_cast<char*>(s.work->p) + 8, 0, 8, s.stream));
+        GCHECK(cudaMemsetAsync(reinterpret_cast<int*>(s.work->p) + 4, 0, sizeof(int), s.stream));
     }
+    int bdone_base = 0;  // IPC boundary-unit counter (int 4 of the work block), per step
     for (size_t pidx = 0; pidx < plan.size(); ++pidx) {
         const Pass& ps = plan[pidx];
         const Variant* var = pass_variant(h, ps.tb);
@@ -1691,6 +1700,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             }
         }
         st.n_passes++;
+        bool kernel_signalled = false;  // IPC: the pass's kernel writes the neighbours' flags
         for (size_t g = 0; g < h.slabs.size(); ++g) {
             Slab& s = h.slabs[g];
             GCHECK(cudaSetDevice(s.device));
@@ -1702,8 +1712,36 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             }
             p.work_base = int(work_base[g]);
             work_base[g] += p.units;
-            if (lk.strip > 0 && !h.instr.on) p.ustrip = lk.strip;
-            if (lk.blk > 0 && var->cy == 1 && !h.instr.on && p.units > li.grid) {
+            const bool ipc_flags = h.ipc && var->cy == 1 && !h.instr.on;
+            if (ipc_flags) {
+                // boundary chunk rows first; the kernel writes the neighbours' flags when they
+                // are done (ipc_after_pass then only counts the epoch)
+                const int hz = std::max(h.hz, ps.tb * h.R);
+                int lo = 0, hi = 0;
+                for (int c = 0; c < p.nzc; ++c) {
+                    const int za = p.zout_lo + c * p.zc_len;
+                    const int zb = std::min(za + p.zc_len, p.zout_hi);
+                    if (h.peer[0].open && za < p.zout_lo + hz) lo = c + 1;
+                    if (h.peer[1].open && zb > p.zout_hi - hz && hi == 0) hi = p.nzc - c;
+                }
+                if (lo + hi >= p.nzc) {  // thin slab: every unit is a boundary unit
+                    lo = hi = 0;
+                    p.bflag_n = p.units;
+                } else {
+                    p.bflag_n = (lo + hi) * p.tiles_x * p.tiles_y;
+                }
+                p.zb_lo = lo;
+                p.zb_hi = hi;
+                p.bdone = reinterpret_cast<int*>(s.work->p) + 4;
+                p.bdone_base = bdone_base;
+                bdone_base += p.bflag_n;
+                p.bflag_dn = h.peer[0].open ? h.peer[0].flags + 1 : nullptr;
+                p.bflag_up = h.peer[1].open ? h.peer[1].flags + 0 : nullptr;
+                p.bflag_val = int(h.epoch + 1);
+                kernel_signalled = true;
+            }
+            if (lk.strip > 0 && !h.instr.on && !ipc_flags) p.ustrip = lk.strip;
+            if (lk.blk > 0 && var->cy == 1 && !h.instr.on && p.units > li.grid && !ipc_flags) {
                 if (lock_base[g] > (1ull << 62)) {
                     GCHECK(cudaMemsetAsync(reinterpret_cast<char*>(s.work->p) + 8, 0, 8, s.stream));
                     lock_base[g] = 0;
@@ -1713,7 +1751,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
                 p.lock_blk = lk.blk;
                 p.lock_slack = lk.slack;
                 lock_base[g] += (unsigned long long)li.grid << 32;  // 2^32 arrivals per CTA
-                if (lk.group) p.ugroup = li.grid;
+                if (lk.group) p.ugroup = li.grid;  // (never with ipc_flags: order is by z rows)
             }
             const CUtensorMap& vmap = tensor_map(h, int(g), s.buf[ps.src]->p, 1, var->lx, var->ly);
             const CUtensorMap* cmap = &vmap;
@@ -1756,7 +1794,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         // halo exchange of the levels the next pass reads: pushed by the pass itself
         // (single-process slabs; the next pass only waits for its neighbours), or copied
         if (h.ipc) {
-            ipc_after_pass(h);
+            ipc_after_pass(h, kernel_signalled);
         } else if (h.push_peers) {
             order_slabs(h);
         } else if (h.slabs.size() > 1 || h.nranks > 1) {

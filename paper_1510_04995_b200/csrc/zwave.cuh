@@ -144,6 +144,19 @@ struct PassParams {
     // tiles, y fastest inside a strip, so y-neighbour tiles are W draws apart instead of a whole
     // tile row (units drawn close together start close together and share L2 halo rows)
     int ustrip;
+    // Multi-process z-slabs (IPC halo push): boundary chunk rows first. The zb_lo bottom and zb_hi
+    // top z-chunk rows of the slab (the units that read the neighbours' pushed halo planes or push
+    // planes into the neighbours' halos) are drawn before the interior rows, and when the last of
+    // those bflag_n units has finished, its CTA writes bflag_val into the neighbours' pass flags
+    // (peer memory, system-scope release after every pushing CTA's fence). A neighbour's next
+    // pass then waits only for this pass's boundary units; the interior units overlap it.
+    int zb_lo, zb_hi;
+    int bflag_n;           // boundary units (the first bflag_n units of the pass); 0 = off
+    int* bdone;            // finished boundary units, cumulative over a step from bdone_base
+    int bdone_base;
+    int* bflag_dn;         // neighbour flag entries to write (peer memory) or null
+    int* bflag_up;
+    int bflag_val;
 };
 
 // Pass chaining. One launch may run a sequence of passes over the same tile grid. Units are
@@ -342,6 +355,10 @@ __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
         const int r = u / p.tiles_x;
         g.ty = r % p.tiles_y;
         zc = r / p.tiles_y;
+        if (p.zb_lo + p.zb_hi > 0) {  // boundary rows first: bottom rows, top rows, interior
+            if (zc >= p.zb_lo) zc = zc < p.zb_lo + p.zb_hi ? p.nzc - p.zb_hi + (zc - p.zb_lo)
+                                                           : zc - p.zb_hi;
+        }
     }
     g.za = p.zout_lo + zc * p.zc_len;
     g.zb = min(g.za + p.zc_len, p.zout_hi);
@@ -1427,6 +1444,25 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 return true;
             };
             unroll_phases<0, NPH>(phase);
+        }
+        if constexpr (!CHAIN && CY == 1) {
+            // IPC z-slabs: the last boundary unit of the pass signals the neighbours
+            if (p.bflag_n > 0 && u < p.bflag_n) {
+                __syncthreads();  // every thread's peer stores of this unit are issued
+                if (tid == 0) {
+                    __threadfence_system();  // cumulative: the CTA's pushes before the count
+                    const int old = atomicAdd(p.bdone, 1);
+                    if (old == p.bdone_base + p.bflag_n - 1) {
+                        __threadfence_system();  // every pushing CTA's stores before the flags
+                        if (p.bflag_dn)
+                            asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p.bflag_dn),
+                                         "r"(p.bflag_val) : "memory");
+                        if (p.bflag_up)
+                            asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p.bflag_up),
+                                         "r"(p.bflag_val) : "memory");
+                    }
+                }
+            }
         }
     }
     if constexpr (PACE) {

@@ -18,10 +18,13 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = int(os.environ.get("GIRIH_IPC_DEVICE", "0"))
     bad = 0
-    for kind, (nx, ny, nz), steps in ((1, (40, 33, 50), 9), (3, (37, 30, 52), 5),
-                                      (2, (36, 29, 48), 6), (0, (41, 35, 47), 7)):
+    # (the last two: slabs of several z-chunk rows, so boundary rows run first and interior
+    # rows overlap the neighbours' next pass; the kernel signals the neighbours)
+    for kind, (nx, ny, nz), steps, zc in ((1, (40, 33, 50), 9, 0), (3, (37, 30, 52), 5, 0),
+                                          (2, (36, 29, 48), 6, 0), (0, (41, 35, 47), 7, 0),
+                                          (1, (70, 45, 150), 7, 6), (3, (45, 38, 160), 4, 7)):
         grid = g.GridSpec(nx, ny, nz, 0)
-        cfg = g.GpuConfig(device=dev)
+        cfg = g.GpuConfig(device=dev, zchunks=zc)
         with g.DeviceState.slab_seeded(kind, grid, 17, True, rank, world, None, cfg) as ds:
             blobs = [None] * world
             dist.all_gather_object(blobs, ds.ipc_export())
