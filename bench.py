@@ -11,6 +11,10 @@ C2 (var7pt 512^3, 100 steps): --n 512 --nt 100; other kinds: --stencil.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--stencil var7pt --n 1024]
 
+At N = 1 the on-device auto-tuner (girih_gpu_tune: model-pruned hill-climb over the compiled
+variants, z chunks and pass chaining, starting from the default) runs first and the timed steps
+use its choice, recorded under gpu.tuned (--no-tune: the defaults).
+
 Prints ONE JSON line (rank 0). `value` is device-timed MLUP/s with inputs resident in HBM;
 `e2e` is the same metric through the drop-in C-ABI call girih_gpu_run on PAGEABLE host buffers
 (what the reference's ProblemState std::vectors are): H2D of u, v, coefficients + all passes +
@@ -315,7 +319,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     tuned = None
     if args.tune:
         if world > 1:  # a slab handle cannot tune alone (girih_gpu_tune refuses it)
-            tuned = {"skipped": "--tune is single-GPU only"}
+            tuned = {"skipped": "the tuner runs on single-GPU handles only (N > 1: defaults)"}
         else:
             tcfg, tml, nmeas = ds.tune(max_tb=args.tb if args.tb > 0 else 0)
             tcfg.device = dev
@@ -445,7 +449,9 @@ def main():
     ap.add_argument("--halo", default="push", choices=["push", "nccl"],
                     help="N > 1: passes push halos into the neighbours' memory (CUDA IPC) or "
                          "exchange them over NCCL after every pass")
-    ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--tune", action="store_true", default=True,
+                    help="run girih_gpu_tune first and time its choice (default on; N = 1 only)")
+    ap.add_argument("--no-tune", dest="tune", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
