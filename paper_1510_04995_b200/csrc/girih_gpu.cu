@@ -3133,8 +3133,20 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         // start at the configuration the handle would run by default, so the search can only
         // move to a measured improvement over it
         const int def_tb = cfg_saved.tb > 0 ? cfg_saved.tb : default_tb_for(h);
-        const int def_var = global_index_of(def_tb <= tb_cap ? pass_variant(h, def_tb)
-                                                             : select_variant(h.kind, tb_cap, -1));
+        // the auto policy's chaining decision (do_step): chained runs use the chain variant
+        const long long cells = (long long)h.nx * h.ny * h.nz;
+        const bool def_chain = h.slabs.size() == 1 && h.nranks == 1 &&
+                               (cfg_saved.chain > 0 ||
+                                (cfg_saved.chain == 0 &&
+                                 cells <= (h.kind == K_VAR7 ? (1ll << 21) : (1ll << 24))));
+        const Variant* def_v = def_tb <= tb_cap ? pass_variant(h, def_tb)
+                                                : select_variant(h.kind, tb_cap, -1);
+        if (def_chain && def_tb <= tb_cap) {
+            const Variant* cv = select_chain_variant(h.kind, def_tb,
+                                                     cfg_saved.variant >= 0 ? cfg_saved.variant : -1);
+            if (cv) def_v = cv;
+        }
+        const int def_var = global_index_of(def_v);
         std::vector<int> vars;
         for (auto& sc : scored)
             if (sc.first >= 0.5 * top || sc.second == def_var) vars.push_back(sc.second);
@@ -3146,6 +3158,7 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         // chain
         const int copts[] = {-1, 1};
         const int nc_opts = (h.slabs.size() == 1 && h.nranks == 1) ? 2 : 1;
+        const int def_c = def_chain ? 1 : 0;  // index into copts of the default's scheduling
         std::map<std::array<int, 3>, double> seen;
         // adaptive_measure (tuner.cpp:47-71): double the test size until two runs agree
         auto measure = [&](int vi, int zi, int ci) -> double {
@@ -3180,7 +3193,7 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         // hill_climb (tuner.cpp:73-104): axis-aligned, strict improvement, memoised
         int bv = int(std::find(vars.begin(), vars.end(), def_var) - vars.begin());
         int bz = 0;
-        int bc = 0;  // one launch per pass (the auto policy's large-grid choice)
+        int bc = def_c;  // the default's scheduling (auto policy: chained on small grids)
         double bs = measure(bv, bz, bc);
         while (true) {
             int nv2 = bv, nz2 = bz, nc2 = bc;
