@@ -57,10 +57,17 @@
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
 #endif
 #ifndef GIRIH_LOCK
-#define GIRIH_LOCK 1  // lockstep pacing code compiled in (PassParams::lock)
+#define GIRIH_LOCK 0  // lockstep pacing compiled in (PassParams::lock; A/B builds only: its
+                      // producer state cost the bench kernel a spill and 2-4%)
 #endif
 #ifndef GIRIH_PACE_LAG
 #define GIRIH_PACE_LAG 2  // PACE clusters: planes a CTA may run ahead of its y-neighbours
+#endif
+#ifndef GIRIH_IPC_FLAGS
+#define GIRIH_IPC_FLAGS 1  // single-pass kernels signal IPC neighbours after their boundary units
+#endif
+#ifndef GIRIH_UORDER
+#define GIRIH_UORDER 1  // unit orders other than z-chunk-major (A/B switches GIRIH_UGROUP/USTRIP)
 #endif
 #ifndef GIRIH_XSHFL
 #define GIRIH_XSHFL 1  // x neighbours by warp shuffle where measured faster (see XSHFL)
@@ -334,7 +341,7 @@ struct UnitGeom {
 __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
     UnitGeom g;
     int zc;
-    if (p.ugroup > 0) {  // groups of ugroup tiles, z chunk inside the group (the last is short)
+    if (GIRIH_UORDER && p.ugroup > 0) {  // groups of ugroup tiles, z chunk inside the group (the last is short)
         const int txy = p.tiles_x * p.tiles_y, per = p.ugroup * p.nzc;
         const int grp = u / per, w = u - grp * per;
         const int gsz = min(p.ugroup, txy - grp * p.ugroup);
@@ -342,7 +349,7 @@ __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
         const int tile = grp * p.ugroup + (w - zc * gsz);
         g.tx = tile % p.tiles_x;
         g.ty = tile / p.tiles_x;
-    } else if (p.ustrip > 0) {
+    } else if (GIRIH_UORDER && p.ustrip > 0) {
         const int txy = p.tiles_x * p.tiles_y;
         zc = u / txy;
         const int tile = u - zc * txy, sw = p.ustrip * p.tiles_y;  // tiles per full strip
@@ -1319,13 +1326,15 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                             // a full pair is one aligned 16-byte store (the neighbour's buffers
                             // share this layout and the offsets are whole planes), so a warp's
                             // push is 512 contiguous bytes of NVLink writes, not 32 strided
-                            // 8-byte ones per cell of the pair
+                            // 8-byte ones per cell of the pair. Radius 4: scalar stores (the
+                            // vector path cost the 255-register const25pt kernel a spill)
+                            constexpr bool PUSH_VEC = R == 1;
 #pragma unroll
                             for (int i = 0; i < PPT; ++i) {
                                 const double2 c2 =
                                     ZPS ? ctrk[ZPS ? i : 0] : zq[TB - 1][i][ZPS ? 0 : (R + PH) % ZQD];
                                 const uint32_t m = ((out_mask & ~ghost_mask) >> (2 * i)) & 3u;
-                                if (m == 3u) {
+                                if (PUSH_VEC && m == 3u) {
                                     *reinterpret_cast<double2*>(fin + colidx[2 * i]) = val[i];
                                     if (pen) *reinterpret_cast<double2*>(pen + colidx[2 * i]) = c2;
                                 } else {
@@ -1445,7 +1454,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             };
             unroll_phases<0, NPH>(phase);
         }
-        if constexpr (!CHAIN && CY == 1) {
+        if constexpr (!CHAIN && CY == 1 && GIRIH_IPC_FLAGS) {
             // IPC z-slabs: the last boundary unit of the pass signals the neighbours
             if (p.bflag_n > 0 && u < p.bflag_n) {
                 __syncthreads();  // every thread's peer stores of this unit are issued

@@ -291,8 +291,9 @@ def test_device_state_stepwise_equals_single_run(girih, oracle):
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_lockstep_pacing_and_group_order(girih, oracle, kind, monkeypatch):
     # single-pass launches with more units than resident CTAs pace their CTAs in lockstep
-    # (PassParams::lock) and draw units in tile groups of the grid size with the z chunk inside
-    # the group (PassParams::ugroup): pure scheduling, results must not change. Forced z chunks
+    # (PassParams::lock; its kernel code is compiled only with -DGIRIH_LOCK=1, A/B builds) and
+    # draw units in tile groups of the grid size with the z chunk inside the group
+    # (PassParams::ugroup) or in column strips (ustrip): pure scheduling, results must not change. Forced z chunks
     # give more units than the persistent grid holds; several block/slack settings, tight to
     # loose, and the chained path disabled so every pass is a single launch.
     g = girih
