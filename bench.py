@@ -453,7 +453,8 @@ def main():
                     help="run girih_gpu_tune first and time its choice (default on; N = 1 only)")
     ap.add_argument("--no-tune", dest="tune", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3,
+                    help="timed drop-in calls after one warm-up call (mean reported)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=8.0)
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
