@@ -415,6 +415,12 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                      "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": hbm_src, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": local_cells * B1[kind] * passes_per_launch,
+                     # ncu code balance: measured DRAM bytes per LUP of the profiled launch
+                     # (algorithmic: B1 / TB), and its excess over the algorithmic bytes
+                     "ncu_bytes_per_lup": (traffic / (local_cells * r0.tb_used * passes_per_launch)
+                                           if traffic else None),
+                     "traffic_over_algorithmic": (traffic / (local_cells * B1[kind] * passes_per_launch)
+                                                  if traffic else None),
                      "avg_launch_ms": avg_launch * 1e3,
                      "lup_roofline_mlups": world * hbm * 1e9 * r0.tb_used / B1[kind] / 1e6,
                      "frac_of_lup_roofline": value / (world * hbm * 1e9 * r0.tb_used / B1[kind] / 1e6),
