@@ -271,7 +271,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
     dev = 0 if shared else local_rank
     tdev = "cpu" if shared else "cuda"  # device of the small plumbing tensors
     hbm, hbm_src = measured_peaks()
-    cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant)
+    cfg = g.GpuConfig(tb=args.tb, device=dev, zchunks=args.zchunks, variant=args.variant,
+                      chain=args.chain)
     dist = None
     halo = None
     ggrid = g.GridSpec(n, n, n)  # the global grid: fixed for every N (strong scaling)
@@ -452,6 +453,8 @@ def main():
     ap.add_argument("--tb", type=int, default=0)
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--zchunks", type=int, default=0)
+    ap.add_argument("--chain", type=int, default=0,
+                    help="pass chaining: 0 auto (grids <= 256^3), 1 always, -1 never")
     ap.add_argument("--halo", default="push", choices=["push", "nccl"],
                     help="N > 1: passes push halos into the neighbours' memory (CUDA IPC) or "
                          "exchange them over NCCL after every pass")
