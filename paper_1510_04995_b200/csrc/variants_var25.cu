@@ -8,6 +8,10 @@ const Variant kVariantsVar25[] = {
     GIRIH_VARIANT(K_VAR25, 1, 32, 16, 64, 1, 1, 2),
     GIRIH_VARIANT(K_VAR25, 1, 32, 32, 128, 2, 1, 1),
     GIRIH_VARIANT_D(K_VAR25, 1, 32, 16, 64, 1, 1, 2),
+    // two fused steps: what the SMEM working set allows at radius 4 (13 coefficient planes
+    // reused R iterations later, no coefficient prefetch, 16x4 output per 32x20 box); measured
+    // to show why var25pt stays single-step
+    GIRIH_VARIANT(K_VAR25, 2, 32, 20, 192, 1, 0, 1),
 };
 const int kNumVariantsVar25 = sizeof(kVariantsVar25) / sizeof(kVariantsVar25[0]);
 
