@@ -707,3 +707,22 @@ def test_handles_on_concurrent_host_threads(girih, oracle):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("seed", [0, 1, 7])
+def test_survey_seeds_every_kind(girih, oracle, seed):
+    # seeds {0, 1, 7} beside the default 42, remapped inputs, default
+    # configuration, through the drop-in call and the device-resident handle
+    g = girih
+    for kind in range(4):
+        base = oracle.init_state(kind, 48, 41, 52, 1, seed, remap=True)
+        ref = base.copy()
+        oracle.naive_sweep(ref, 12)
+        st = to_problem(g, base)
+        g.run(st, 12)
+        assert_state_equal(st, ref, f"{KIND_IDS[kind]} seed {seed} drop-in")
+        with g.DeviceState.from_state(to_problem(g, base)) as ds:
+            ds.step(5)
+            ds.step(7)
+            out = ds.download()
+        assert_state_equal(out, ref, f"{KIND_IDS[kind]} seed {seed} handle")
