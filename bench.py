@@ -319,8 +319,26 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
         ds = g.DeviceState.seeded(kind, ggrid, 42, remap=True, config=cfg)
     tuned = None
     if args.tune:
-        if world > 1:  # a slab handle cannot tune alone (girih_gpu_tune refuses it)
-            tuned = {"skipped": "the tuner runs on single-GPU handles only (N > 1: defaults)"}
+        if world > 1:
+            # a slab handle cannot tune alone (its passes wait on its neighbours; girih_gpu_tune
+            # refuses it): rank 0 tunes a single-GPU handle of one slab's size and every rank
+            # takes that configuration (broadcast), so all ranks run the same pass sequence
+            import torch
+            vec = torch.zeros(4, dtype=torch.float64, device=tdev)
+            ml, nmeas = 0.0, 0
+            if rank == 0:
+                sgrid = g.GridSpec(n, n, max(2 * (4 if kind >= 2 else 1) + 1, n // world))
+                with g.DeviceState.seeded(kind, sgrid, 42, remap=True,
+                                          config=g.GpuConfig(device=dev)) as tds:
+                    tcfg, ml, nmeas = tds.tune(max_tb=args.tb if args.tb > 0 else 0)
+                g.trim()
+                vec[0], vec[1], vec[2], vec[3] = tcfg.tb, tcfg.variant, tcfg.zchunks, tcfg.chain
+            dist.broadcast(vec, 0)
+            tb_, var_, zc_, ch_ = (int(x) for x in vec.cpu().tolist())
+            ds.set_config(g.GpuConfig(tb=tb_, variant=var_, zchunks=zc_, chain=ch_, device=dev))
+            tuned = {"tb": tb_, "variant": var_, "zchunks": zc_, "chain": ch_,
+                     "tuned_on": f"rank 0, single-GPU {n}x{n}x{n // world} (one slab), broadcast",
+                     "mlups": ml if rank == 0 else None, "measured": nmeas}
         else:
             tcfg, tml, nmeas = ds.tune(max_tb=args.tb if args.tb > 0 else 0)
             tcfg.device = dev

@@ -673,6 +673,8 @@ def test_bench_multirank_path_functional(girih):
     assert d["n_gpus"] == 2 and d["value"] > 0 and "NOT a measurement" in d["data"]
     assert d["scaling"] == "strong" and d["gpu"]["global_grid"] == [256, 256, 256]
     assert "pushed by each pass" in d["gpu"]["parallelism"]
+    # the tuner ran on rank 0 on a one-slab single-GPU handle and every rank took its choice
+    assert "broadcast" in d["gpu"]["tuned"]["tuned_on"] and d["gpu"]["tuned"]["tb"] >= 1
     # rank 0's drop-in call on pageable host buffers
     assert d["e2e"]["value"] > 0 and "pageable" in d["e2e"]["host_memory"]
 
