@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GIRIH_GPU_ABI_VERSION 4
+#define GIRIH_GPU_ABI_VERSION 5
 
 #define GIRIH_OK 0
 #define GIRIH_EINVAL (-1)
@@ -107,6 +107,8 @@ typedef struct {
     int direct_out;         /* 1: output stored from registers (no smem staging + TMA store) */
     int paced;              /* 1: cluster of independent y-neighbour tiles kept on the same z
                                plane by a per-plane cluster barrier (shared rows hit L2) */
+    int narrow;             /* x halo XO > 0: the threads compute only the lx - 2 XO output
+                               columns of the lx-wide box (single-step kernels); 0: all lx */
 } girih_gpu_variant;
 
 const char* girih_gpu_last_error(void);

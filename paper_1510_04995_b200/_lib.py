@@ -61,7 +61,7 @@ class GirihGpuVariant(C.Structure):
     _fields_ = [("kind", C.c_int), ("tb", C.c_int), ("lx", C.c_int), ("ly", C.c_int),
                 ("threads", C.c_int), ("prefetch", C.c_int), ("smem_bytes", C.c_int),
                 ("cluster_y", C.c_int), ("aux_prefetch", C.c_int), ("direct_out", C.c_int),
-                ("paced", C.c_int)]
+                ("paced", C.c_int), ("narrow", C.c_int)]
 
 
 class GirihGpuTraceRecord(C.Structure):

@@ -182,8 +182,10 @@ const Variant* select_chain_variant(int kind, int tb, int requested) {
 // 127.3 K vs 125.6 K, 512^3 136.4 K vs 130.5 K, 768^3 141.2 K vs 132.4 K; 1024^3 136.2-137.4 K vs
 // 128.6-133.6 K; profiles/r2_default_variant_ab.txt)
 // const7pt TB = 1 single-pass launches likewise take the direct-output 64x10 tile (256^3 225 K vs
-// 198 K, 384^3 309 K vs 267 K, 512^3 325 K vs 288 K); chained launches keep the staged tile
-// (select_chain_variant: 256^3 281 K vs 273 K).
+// 198 K, 384^3 309 K vs 267 K, 512^3 325 K vs 288 K; at 512^3 it also beats the 68-column
+// output-only tiles, 374-380 K vs 356-362 K: the pass is DRAM-bound there and 544-byte box rows
+// cost sectors); chained launches take the table's first entry, the output-columns-only 68x18
+// tile (select_chain_variant).
 const Variant* default_variant(int kind, int tb, long long plane_cells) {
     (void)plane_cells;
     int n;
@@ -192,7 +194,8 @@ const Variant* default_variant(int kind, int tb, long long plane_cells) {
         if (t[i].tb != tb || !t[i].direct_out || t[i].cy != 1) continue;
         if (kind == K_VAR7 && tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].aux_prefetch == 2)
             return &t[i];
-        if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10) return &t[i];
+        if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10 && !t[i].narrow)
+            return &t[i];
     }
     return select_variant(kind, tb, -1);
 }
@@ -1208,6 +1211,11 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     const int R = h.R, H = tb * R;
     // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
     t.hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
+    if (var->narrow > 0) {  // the kernel's threads sit on the box's inner columns [XO, lx - XO)
+        if ((h.off + R - var->narrow) % 2 != 0)
+            throw_err(GIRIH_EINVAL, "this variant's x halo needs the default row offset");
+        t.hx = var->narrow;
+    }
     t.ox = var->lx - 2 * t.hx;
     // y: one tile = one CTA, or one cluster of cy CTAs whose boxes overlap by 2R rows and
     // share the fused levels' halo rows (zwave.cuh ZwaveConfig::OYC)
@@ -1229,7 +1237,8 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     // nzl + 2 nzc (TB-s) R planes
     t.computed_lups = 0;
     for (int lev = 1; lev <= tb; ++lev) {
-        const long long ex = (long long)(t.ox + 2 * (t.hx - lev * R));
+        const long long ex = var->narrow > 0 ? (long long)t.ox  // output columns only
+                                              : (long long)(t.ox + 2 * (t.hx - lev * R));
         const long long ey = (long long)(t.oy + 2 * (tb - lev) * R);
         const long long ez = (long long)nzl + 2LL * t.nzc * (tb - lev) * R;
         t.computed_lups += ex * ey * (long long)txy * ez;
@@ -1468,12 +1477,12 @@ void ipc_after_pass(Handle& h, bool kernel_signalled = false) {
     }
 }
 
-// Default fused depth: the kind's, except const7pt grids of at most 128^3 cells, whose chained
-// two-step passes do more work per unit (64^3: 33.5 K vs 23.7 K MLUP/s, 128^3: 130 K vs 109 K;
-// 256^3 and up: one step, 282 K vs 247 K; tools/tb_sweep.sh)
+// Default fused depth: the kind's, except const7pt grids of at most ~80^3 cells, whose chained
+// two-step passes do more work per unit (64^3: 33.5 K vs 24-26 K MLUP/s; 128^3: 130 K, but the
+// single-step output-columns-only tile reaches 144 K there; 256^3 and up: one step)
 int default_tb_for(const Handle& h) {
     const long long cells = (long long)h.nx * h.ny * h.nz;
-    if (h.kind == K_CONST7 && cells <= (1ll << 21) && h.slabs.size() == 1 && h.nranks == 1)
+    if (h.kind == K_CONST7 && cells <= (1ll << 19) && h.slabs.size() == 1 && h.nranks == 1)
         return 2;
     return kKinds[h.kind].default_tb;
 }
@@ -2466,6 +2475,7 @@ int girih_gpu_variant_info(int index, girih_gpu_variant* out) {
         out->aux_prefetch = v->aux_prefetch;
         out->direct_out = v->direct_out;
         out->paced = v->pace;
+        out->narrow = v->narrow;
     });
 }
 

@@ -26,6 +26,8 @@ struct Variant {
     OccFn occupancy_chain;       // the same for the chained kernel
     int direct_out;              // 1: output level stored straight from registers (no staging)
     int pace;                    // 1: the cluster only paces independent tiles (no shared rows)
+    int narrow;                  // x halo XO > 0: the threads cover only the lx - 2 XO output
+                                 // columns of the box (ZwaveConfig::NARROW); 0 = all lx columns
 };
 
 // one table per kind, defined in variants_<kind>.cu
@@ -156,7 +158,8 @@ cudaError_t occupancy_zwave(int* max_ctas) {
             &launch_zwave_chain<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                       \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                          \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF, true>,                    \
-            ((CF) >> 8) & 1, ((CF) >> 9) & 1                                                  \
+            ((CF) >> 8) & 1, ((CF) >> 9) & 1,                                                 \
+            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::XO                            \
     }
 // CY CTAs per y cluster
 #define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \
@@ -167,6 +170,11 @@ cudaError_t occupancy_zwave(int* max_ctas) {
 // clusters of CY y-neighbour tiles paced in lockstep (ZwaveConfig::PACE), direct output
 #define GIRIH_VARIANT_PD(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \
     GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, (CY) | (1 << 8) | (1 << 9))
+// output-columns-only thread mapping (single-step kernels; LX = computed columns + 2 XO)
+#define GIRIH_VARIANT_N(KIND, TB, LX, LY, NT, P, PA, MINB) \
+    GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, 1 | (1 << 10))
+#define GIRIH_VARIANT_ND(KIND, TB, LX, LY, NT, P, PA, MINB) \
+    GIRIH_VARIANT_F(KIND, TB, LX, LY, NT, P, PA, MINB, 1 | (1 << 8) | (1 << 10))
 #define GIRIH_VARIANT(KIND, TB, LX, LY, NT, P, PA, MINB) \
     GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, 1)
 

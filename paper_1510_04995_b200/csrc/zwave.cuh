@@ -506,6 +506,15 @@ struct ZwaveConfig {
     static constexpr int CY = CF & 255;
     static constexpr bool DOUT = ((CF >> 8) & 1) != 0;
     static constexpr int R = KindTraits<KIND>::R;
+    // NARROW (flag 4, single-step kernels): the threads cover only the LXC = LX - 2 XO output
+    // columns of the box instead of all LX (whose XO edge columns only ever feed neighbours), so
+    // a 64-column warp row is all output: tiles of 64 columns divide the BASELINE grids exactly
+    // (256 = 4 x 64, 512 = 8 x 64) where 60- and 56-column tiles leave a mostly empty last tile
+    // column (256^3 const7pt: 5 x 64 computed columns per row became 4 x 64). XO is the x halo
+    // the host then uses (R = 1: H + 1 = 2 keeps the TMA box origins 16-byte aligned).
+    static constexpr bool NARROW = ((CF >> 10) & 1) != 0;
+    static constexpr int XO = NARROW ? 2 * ((R + 1) / 2) : 0;
+    static constexpr int LXC = LX - 2 * XO;  // columns the threads compute
     static constexpr int Q = 2 * R + 1;     // z window of one level
     // z neighbours come from per-thread register queues; smem only holds the centre planes
     // that other threads read for x/y neighbours: R+1 planes per computed level (written R
@@ -532,21 +541,22 @@ struct ZwaveConfig {
     static constexpr int OYS = SHARE ? OWN : OY;                  // widest output rows of a CTA
     static constexpr int OYC = CY > 1 ? (PACE ? CY * OY : CY * OWN - 2 * (TB - 1) * R) : OY;
     static constexpr int OYE = SHARE ? LY - R - H : OY;           // outer CTAs' output rows
-    static constexpr int OXM = LX - 2 * H;  // widest output tile (x halo = H)
+    static constexpr int OXM = NARROW ? LXC : LX - 2 * H;  // widest output tile (x halo = H)
     static constexpr int CELLS = LX * LY;
+    static constexpr int CELLS_S = round16(CELLS);  // ring slot stride (TMA: 128-byte aligned)
     // threads cover the level-1 valid rows [R, LY - R) only: the R outermost rows of the
     // loaded box are neighbours, never computed (for TB = 1 that is exactly the output rows)
     static constexpr int CR = LY - 2 * R;
-    static constexpr int PPT = CR * LX / (2 * NT);  // x-pairs of cells per thread
+    static constexpr int PPT = CR * LXC / (2 * NT);  // x-pairs of cells per thread
     // STACK (64-wide tiles, >= 2 pairs per thread): a warp owns whole rows and a thread the
     // same pair column in PPT consecutive rows, so the y neighbours of its pairs are one column
     // window of PPT+2R pair loads instead of 2R loads per pair (radius 4: 46% fewer LDS.128)
-    static constexpr bool STACK = LX == 64 && PPT >= 2 && STACK_OK<KIND>::value;
+    static constexpr bool STACK = LXC == 64 && PPT >= 2 && STACK_OK<KIND>::value;
     static constexpr int XA = 2 * ((R + 1) / 2);  // pair-aligned x reach (R=1: 2, R=4: 4)
     static constexpr int NRING = NR0 + (TB - 1) * QL;
     // aux (coefficient) planes: the level-1 area, x origin kept 16-byte aligned
     static constexpr int NAUX = AuxArrays<KIND>::N;
-    static constexpr int AXO = R & ~1, AYO = R;
+    static constexpr int AXO = NARROW ? XO : R & ~1, AYO = R;
     static constexpr int AX = LX - 2 * AXO, AY = LY - 2 * AYO;
     static constexpr int AYX = AX * AY;
     // var7pt with TB = 2 keeps each pair's coefficients in registers from level 1 to level 2
@@ -558,17 +568,18 @@ struct ZwaveConfig {
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
     static constexpr int GUARD = round16(LX * R + R + 8);
     static constexpr int STAGE = DOUT ? 0 : round16(OXM * OYS);  // one output staging plane
-    static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS +
+    static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS_S +
                                            size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
-    static_assert((CR * LX) % (2 * NT) == 0, "computed rows must split evenly into cell pairs");
+    static_assert((CR * LXC) % (2 * NT) == 0, "computed rows must split evenly into cell pairs");
+    static_assert(!NARROW || (TB == 1 && CY == 1), "NARROW: single-step, non-cluster kernels");
     static_assert(NT % 32 == 0, "whole warps");
     static_assert(!STACK || CR % (NT / 32) == 0, "STACK: every warp owns whole rows");
-    static_assert(LX % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
+    static_assert(LXC % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
     static_assert(LX - 2 * H - 2 > 0 && OYE > 0, "tile too small for the halo (x halo may be H+1)");
     static_assert(LX <= 256 && LY <= 256, "TMA box limit");
     static_assert((LX * 8) % 16 == 0 && (AX * 8) % 16 == 0, "TMA inner box must be 16-byte multiple");
-    static_assert((CELLS * 8) % 128 == 0 && (AYX * 8) % 128 == 0, "TMA smem boxes 128-byte aligned");
+    static_assert((CELLS_S * 8) % 128 == 0 && (AYX * 8) % 128 == 0, "TMA smem boxes 128-byte aligned");
     static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
     static_assert(CY == 1 || PACE || (TB >= 2 && OYE > 0 && OWN >= 2 * R && CY <= 16),
                   "clusters share fused-level halo rows: TB >= 2, outer CTAs need output rows");
@@ -589,7 +600,9 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     static_assert(CY == 1 || !CHAIN, "cluster kernels run single passes");
     static_assert(!INSTR || !CHAIN, "instrumented kernels run single passes");
     constexpr int R = CFG::R, QL = CFG::QL, NR0 = CFG::NR0, H = CFG::H;
-    constexpr int CELLS = CFG::CELLS, PPT = CFG::PPT, XA = CFG::XA;
+    constexpr int CELLS = CFG::CELLS, CELLS_S = CFG::CELLS_S, PPT = CFG::PPT, XA = CFG::XA;
+    constexpr bool NARROW = CFG::NARROW;
+    constexpr int XO = CFG::XO, LXC = CFG::LXC;
     constexpr int OWN = CFG::OWN, OYC = CFG::OYC;
     constexpr int NAUX = CFG::NAUX, NAR = CFG::NAR, AXO = CFG::AXO, AYO = CFG::AYO;
     constexpr bool CQ = CFG::CQ;
@@ -617,8 +630,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring0 = reinterpret_cast<double*>(smem_raw) + GUARD;
-    double* ringL = ring0 + NR0 * CELLS;           // level s (1..TB-1): ringL + (s-1)*QL*CELLS
-    double* auxr = ringL + (TB - 1) * QL * CELLS;  // aux planes: NAR x [NAUX][AY][AX]
+    double* ringL = ring0 + NR0 * CELLS_S;           // level s (1..TB-1): ringL + (s-1)*QL*CELLS
+    double* auxr = ringL + (TB - 1) * QL * CELLS_S;  // aux planes: NAR x [NAUX][AY][AX]
     double* stage = auxr + NAR * AUXPLANE + GUARD; // 3 output staging planes [OYS][ox]
     uint64_t* vbar = reinterpret_cast<uint64_t*>(stage + 3 * STAGE);
     uint64_t* abar = vbar + NR0;
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         const int xd = p.off + vcur.ug.tx * p.ox + R - p.hx;  // even by construction
         const int yd = vcur.ug.ty * OYC + crank * OWN + R - H;
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
-        tma_load_plane(ring0 + slot * CELLS, &cd.d[CHAIN ? cd.pidx[vcur.q] : 0].vmap, xd, yd, j,
+        tma_load_plane(ring0 + slot * CELLS_S, &cd.d[CHAIN ? cd.pidx[vcur.q] : 0].vmap, xd, yd, j,
                        &vbar[slot]);
         ++vnext;
         if (CY > 1 && crank > 0)  // cluster members replay the leader's units
@@ -833,7 +846,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
         // first cell of the pair (even)
-        const int c = CFG::STACK ? (R + (tid >> 5) * PPT + i) * LX + 2 * (tid & 31)
+        const int c = CFG::STACK ? (R + (tid >> 5) * PPT + i) * LX + XO + 2 * (tid & 31)
+                      : NARROW   ? (R + 2 * (tid + NT * i) / LXC) * LX + XO + 2 * (tid + NT * i) % LXC
                                  : 2 * (tid + NT * i) + R * LX;
         lcell[i] = c;
         const int lx = c % LX, ly = c / LX;
@@ -1027,13 +1041,13 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             // level-0 newest plane j into the level-0 z queue input (one LDS.128 per pair)
             double2 newest[PPT];  // level s-1 at (pair, k_s + R), produced this iteration
             {
-                const double2* pj = reinterpret_cast<const double2*>(ring0 + (g % NR0) * CELLS);
+                const double2* pj = reinterpret_cast<const double2*>(ring0 + (g % NR0) * CELLS_S);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) newest[i] = pj[lcell[i] >> 1];
             }
             double2 ctrk[ZPS ? PPT : 1];  // ZPS: level 0 at the centre plane k = j - R
             if constexpr (ZPS) {
-                const double2* pk = reinterpret_cast<const double2*>(ring0 + ((g - R) % NR0) * CELLS);
+                const double2* pk = reinterpret_cast<const double2*>(ring0 + ((g - R) % NR0) * CELLS_S);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) ctrk[i] = pk[lcell[i] >> 1];
             }
@@ -1072,8 +1086,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
                 // centre plane k of level s-1 (x/y neighbours, other threads' values)
                 const double2* pc = reinterpret_cast<const double2*>(
-                    s == 1 ? ring0 + ((g - R) % NR0) * CELLS
-                           : ringL + ((s - 2) * QL + (k + KOFF) % QL) * CELLS);
+                    s == 1 ? ring0 + ((g - R) % NR0) * CELLS_S
+                           : ringL + ((s - 2) * QL + (k + KOFF) % QL) * CELLS_S);
                 const double2* aux = NAUX > 0 ? reinterpret_cast<const double2*>(
                                                     auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE)
                                               : nullptr;
@@ -1112,6 +1126,15 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                             xs[2 * t] = d == 0 ? ctr.x : __shfl_sync(0xffffffffu, ctr.x, lane + d);
                             xs[2 * t + 1] =
                                 d == 0 ? ctr.y : __shfl_sync(0xffffffffu, ctr.y, lane + d);
+                            if constexpr (NARROW) {
+                                // every column is an output column: the row's edge lanes take
+                                // the pair beyond the warp's row from the box
+                                if (d != 0 && (lane + d < 0 || lane + d > 31)) {
+                                    const double2 w = pc[h2 + d];
+                                    xs[2 * t] = w.x;
+                                    xs[2 * t + 1] = w.y;
+                                }
+                            }
                         }
                     } else {
 #pragma unroll
@@ -1134,7 +1157,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         if (dz == R) return newest[i];
                         if (ZPS && dz > 0)
                             return reinterpret_cast<const double2*>(
-                                ring0 + ((g - R + dz) % NR0) * CELLS)[lcell[i] >> 1];
+                                ring0 + ((g - R + dz) % NR0) * CELLS_S)[lcell[i] >> 1];
                         return zq[s - 1][i][(dz + R + PH) % ZQD];
                     };
                     auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
@@ -1358,7 +1381,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
             for (int L = 1; L < TB; ++L) {
                 if (ring_slot[L] < 0) continue;
-                double2* wr = reinterpret_cast<double2*>(ringL + ((L - 1) * QL + ring_slot[L]) * CELLS);
+                double2* wr = reinterpret_cast<double2*>(ringL + ((L - 1) * QL + ring_slot[L]) * CELLS_S);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) wr[lcell[i] >> 1] = fresh[L][i];
                 if constexpr (CY > 1) {

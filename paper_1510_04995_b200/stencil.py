@@ -155,7 +155,7 @@ def variants():
         out.append(dict(index=i, kind=v.kind, tb=v.tb, lx=v.lx, ly=v.ly, threads=v.threads,
                         prefetch=v.prefetch, smem_bytes=v.smem_bytes, cluster_y=v.cluster_y,
                         aux_prefetch=v.aux_prefetch, direct_out=v.direct_out,
-                        paced=v.paced))
+                        paced=v.paced, narrow=v.narrow))
     return out
 
 

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(girih):
 
 
 def test_abi_version(girih):
-    assert girih.load().girih_gpu_abi_version() == 4
+    assert girih.load().girih_gpu_abi_version() == 5
 
 
 def test_traits_and_names(girih):
@@ -49,7 +49,7 @@ def test_variants_registry(girih):
         assert v["smem_bytes"] <= 227 * 1024
         R = 1 if v["kind"] < 2 else 4
         # threads cover the level-1 rows [R, ly - R) in x-pairs
-        assert v["lx"] * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
+        assert (v["lx"] - 2 * v["narrow"]) * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
         assert v["lx"] > 2 * R * v["tb"]
         if v["cluster_y"] == 1:
             assert v["ly"] > 2 * R * v["tb"]

@@ -97,6 +97,27 @@ def test_every_variant(girih, oracle, kind):
         assert_state_equal(st, ref, f"variant {v}")
 
 
+def test_narrow_variants(girih, oracle):
+    # output-columns-only tiles (ZwaveConfig::NARROW): several 64-column tiles per row with a
+    # partial last one and odd extents, per-pass and chained launches, forced z chunks,
+    # emulated slabs and an odd start level
+    g = girih
+    vs = [v for v in g.variants() if v["narrow"]]
+    assert vs, "no NARROW variant compiled"
+    for v in vs:
+        kind = v["kind"]
+        base = oracle.init_state(kind, 141, 37, 21, 1, 11 + v["index"], remap=True)
+        oracle.naive_sweep(base, 1)
+        ref = base.copy()
+        oracle.naive_sweep(ref, 5)
+        for cfg in (g.GpuConfig(tb=1, variant=v["index"], chain=-1),
+                    g.GpuConfig(tb=1, variant=v["index"], chain=1, zchunks=3),
+                    g.GpuConfig(tb=1, variant=v["index"], emulate_slabs=2)):
+            st = to_problem(g, base)
+            g.run(st, 5, cfg)
+            assert_state_equal(st, ref, f"variant {v} cfg {cfg}")
+
+
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_cluster_variants(girih, oracle, kind):
     # thread-block clusters along y (the fused levels' halo rows shared through distributed
