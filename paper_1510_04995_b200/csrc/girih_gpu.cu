@@ -186,16 +186,24 @@ const Variant* select_chain_variant(int kind, int tb, int requested) {
 // output-only tiles, 374-380 K vs 356-362 K: the pass is DRAM-bound there and 544-byte box rows
 // cost sectors); chained launches take the table's first entry, the output-columns-only 68x18
 // tile (select_chain_variant).
-const Variant* default_variant(int kind, int tb, long long plane_cells) {
-    (void)plane_cells;
+// var7pt TB = 2: where the 62-column inner-columns-only tile (68-column box, its grid starting on
+// the ghost column) needs fewer tile columns than the 60-column one, it is the default (1024:
+// 17 instead of 18; same box, fresh processes: 138.6 K vs 137.0 K MLUP/s, DRAM reads 85.5 vs
+// 87.5 GB per pass); elsewhere it is equal or up to 1% slower (512^3: 134.6 K vs 136.2 K).
+const Variant* default_variant(int kind, int tb, int nx) {
     int n;
     const Variant* t = variant_table(kind, &n);
+    if (kind == K_VAR7 && tb == 2 && (nx + 1 + 61) / 62 < (nx + 59) / 60) {
+        for (int i = 0; i < n; ++i)
+            if (t[i].tb == 2 && t[i].narrow && t[i].lx == 68 && t[i].ly == 18 &&
+                t[i].aux_prefetch == 2 && t[i].cy == 1)
+                return &t[i];
+    }
     for (int i = 0; i < n; ++i) {
-        if (t[i].tb != tb || !t[i].direct_out || t[i].cy != 1) continue;
+        if (t[i].tb != tb || !t[i].direct_out || t[i].cy != 1 || t[i].narrow) continue;
         if (kind == K_VAR7 && tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].aux_prefetch == 2)
             return &t[i];
-        if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10 && !t[i].narrow)
-            return &t[i];
+        if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10) return &t[i];
     }
     return select_variant(kind, tb, -1);
 }
@@ -1188,6 +1196,7 @@ int max_resident_ctas(const Variant* var, bool chained = false) {
 // it evaluates (shared by build_params and the analytic model girih_gpu_model).
 struct TileGeom {
     int hx, ox, oy, tiles_x, tiles_y, nzc, zc_len, units;
+    int xorg;  // allocated x of local column 0 of the first tile column (PassParams::xorg)
     long long computed_lups;
 };
 
@@ -1211,10 +1220,18 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     const int R = h.R, H = tb * R;
     // x halo: H, or H+1 when that makes every tile's TMA x origin (off + R - hx + k*ox) even
     t.hx = ((h.off + R - H) % 2 == 0) ? H : H + 1;
-    if (var->narrow > 0) {  // the kernel's threads sit on the box's inner columns [XO, lx - XO)
-        if ((h.off + R - var->narrow) % 2 != 0)
-            throw_err(GIRIH_EINVAL, "this variant's x halo needs the default row offset");
+    t.xorg = R - t.hx;
+    if (var->narrow > 0) {  // the kernel's threads sit on the box's inner columns
         t.hx = var->narrow;
+        t.xorg = R - t.hx;
+        if ((h.off + t.xorg) % 2 != 0) {
+            // odd TMA origin: start the tile grid one column earlier (its first output column
+            // is then a ghost column, masked). Only direct-output kernels can: a TMA store map
+            // cannot clip below its origin.
+            if (!var->direct_out)
+                throw_err(GIRIH_EINVAL, "this variant's x halo needs the default row offset");
+            t.xorg -= 1;
+        }
     }
     t.ox = var->lx - 2 * t.hx;
     // y: one tile = one CTA, or one cluster of cy CTAs whose boxes overlap by 2R rows and
@@ -1222,7 +1239,8 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     t.oy = var->cy == 1 ? var->ly - 2 * H
            : var->pace  ? var->cy * (var->ly - 2 * H)
                         : var->cy * (var->ly - 2 * R) - 2 * (tb - 1) * R;
-    t.tiles_x = (h.nx + t.ox - 1) / t.ox;
+    // interior columns [0, nx) sit at local output columns from (R - hx) - xorg on (0 or 1)
+    t.tiles_x = (h.nx + (R - t.hx - t.xorg) + t.ox - 1) / t.ox;
     t.tiles_y = (h.ny + t.oy - 1) / t.oy;
     const int txy = t.tiles_x * t.tiles_y;
     // units are per cluster: the z-chunk heuristics count clusters as the resident "CTAs"
@@ -1237,7 +1255,7 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     // nzl + 2 nzc (TB-s) R planes
     t.computed_lups = 0;
     for (int lev = 1; lev <= tb; ++lev) {
-        const long long ex = var->narrow > 0 ? (long long)t.ox  // output columns only
+        const long long ex = var->narrow > 0 ? (long long)(t.ox + 2 * (tb - 1) * R)  // the threads' columns
                                               : (long long)(t.ox + 2 * (t.hx - lev * R));
         const long long ey = (long long)(t.oy + 2 * (tb - lev) * R);
         const long long ez = (long long)nzl + 2LL * t.nzc * (tb - lev) * R;
@@ -1277,6 +1295,7 @@ PassParams build_params(Handle& h, const Pass& ps, const Variant* var, int slab_
     PassParams p{};
     p.hx = hx;
     p.ox = OX;
+    p.xorg = tg.xorg;
     p.src_prev = ps.src_prev >= 0 ? s.buf[ps.src_prev]->p : nullptr;
     p.dst_final = s.buf[ps.dst]->p;
     p.dst_penult = ps.dst_penult >= 0 ? s.buf[ps.dst_penult]->p : nullptr;
@@ -1511,7 +1530,7 @@ const Variant* pass_variant(const Handle& h, int tb) {
         const Variant* v = select_variant(h.kind, tb, h.cfg.variant);
         if (v->tb == tb) return v;
     }
-    return default_variant(h.kind, tb, (long long)h.nx * h.ny);
+    return default_variant(h.kind, tb, h.nx);
 }
 
 StepStats do_step(Handle& h, long long steps, bool time_passes) {

@@ -26,8 +26,9 @@ struct Variant {
     OccFn occupancy_chain;       // the same for the chained kernel
     int direct_out;              // 1: output level stored straight from registers (no staging)
     int pace;                    // 1: the cluster only paces independent tiles (no shared rows)
-    int narrow;                  // x halo XO > 0: the threads cover only the lx - 2 XO output
-                                 // columns of the box (ZwaveConfig::NARROW); 0 = all lx columns
+    int narrow;                  // > 0: the threads cover only the inner columns of the lx-wide
+                                 // box (ZwaveConfig::NARROW) and this is the x halo of the output
+                                 // tile, XO + (TB-1) R; 0 = threads on all lx columns
 };
 
 // one table per kind, defined in variants_<kind>.cu
@@ -159,7 +160,10 @@ cudaError_t occupancy_zwave(int* max_ctas) {
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF>,                          \
             &occupancy_zwave<KIND, TB, LX, LY, NT, P, PA, MINB, CF, true>,                    \
             ((CF) >> 8) & 1, ((CF) >> 9) & 1,                                                 \
-            ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::XO                            \
+            (ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::NARROW                       \
+                 ? ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::XO +                    \
+                       ((TB)-1) * ZwaveConfig<KIND, TB, LX, LY, NT, P, PA, MINB, CF>::R        \
+                 : 0)                                                                          \
     }
 // CY CTAs per y cluster
 #define GIRIH_VARIANT_C(KIND, TB, LX, LY, NT, P, PA, MINB, CY) \

@@ -29,6 +29,11 @@ const Variant kVariantsVar7[] = {
     GIRIH_VARIANT_D(K_VAR7, 2, 64, 18, 512, 2, 2, 1),
     GIRIH_VARIANT_D(K_VAR7, 2, 64, 17, 480, 2, 2, 1),
     GIRIH_VARIANT_PD(K_VAR7, 2, 64, 18, 512, 2, 2, 1, 2),
+    // inner-columns-only tiles: level 1 on all 64 thread columns of a 68-column box, 62 output
+    // columns (1024 = 16.5 x 62: 17 tile columns instead of 18, coefficient boxes 64 wide per
+    // 62 outputs instead of per 60)
+    GIRIH_VARIANT_ND(K_VAR7, 2, 68, 18, 512, 2, 2, 1),
+    GIRIH_VARIANT_ND(K_VAR7, 2, 68, 18, 512, 2, 1, 1),
 };
 const int kNumVariantsVar7 = sizeof(kVariantsVar7) / sizeof(kVariantsVar7[0]);
 

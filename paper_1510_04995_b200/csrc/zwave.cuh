@@ -111,6 +111,10 @@ struct PassParams {
     unsigned long long* ptrace;  // optional per-iteration phase clocks of CTA 0 (debug)
     int hx, ox;              // x halo (H or H+1) and output tile width LX - 2*hx: TMA needs the
                              // innermost box coordinate 16-byte aligned (even for fp64)
+    int xorg;                // allocated x of local column 0 of tile column 0: R - hx, or one less
+                             // when that makes the TMA origins even (output-only tiles with an odd
+                             // halo: the first tile's first output column then sits on the ghost
+                             // column and is masked like any ghost cell)
     // Halo push (single-process z-slabs): the output cells of this slab's bottom / top push_hz
     // own planes are also stored straight into the lower / upper neighbour's halo planes (peer
     // memory over NVLink, or the same device for emulated slabs), so no exchange step follows
@@ -506,12 +510,16 @@ struct ZwaveConfig {
     static constexpr int CY = CF & 255;
     static constexpr bool DOUT = ((CF >> 8) & 1) != 0;
     static constexpr int R = KindTraits<KIND>::R;
-    // NARROW (flag 4, single-step kernels): the threads cover only the LXC = LX - 2 XO output
-    // columns of the box instead of all LX (whose XO edge columns only ever feed neighbours), so
-    // a 64-column warp row is all output: tiles of 64 columns divide the BASELINE grids exactly
-    // (256 = 4 x 64, 512 = 8 x 64) where 60- and 56-column tiles leave a mostly empty last tile
-    // column (256^3 const7pt: 5 x 64 computed columns per row became 4 x 64). XO is the x halo
-    // the host then uses (R = 1: H + 1 = 2 keeps the TMA box origins 16-byte aligned).
+    // NARROW (flag 4): the threads cover only the LXC = LX - 2 XO inner columns of the box
+    // instead of all LX (whose XO edge columns only ever feed neighbours). Single-step kernels:
+    // a 64-column warp row is all output, so tiles of 64 columns divide the BASELINE grids
+    // exactly (256 = 4 x 64, 512 = 8 x 64) where 60- and 56-column tiles leave a mostly empty
+    // last tile column (256^3 const7pt: 5 x 64 computed columns per row became 4 x 64); XO is
+    // the x halo the host then uses (R = 1: H + 1 = 2 keeps the TMA box origins 16-byte
+    // aligned). Fused kernels: level 1 is valid on all LXC columns and the output tile is
+    // LXC - 2 (TB-1) R wide (var7pt TB = 2: 62 columns from a 68-column box instead of 60 from
+    // 64; the x halo XO + (TB-1) R = 3 is odd, so the tile grid starts one column into the ghost
+    // cells, PassParams::xorg).
     static constexpr bool NARROW = ((CF >> 10) & 1) != 0;
     static constexpr int XO = NARROW ? 2 * ((R + 1) / 2) : 0;
     static constexpr int LXC = LX - 2 * XO;  // columns the threads compute
@@ -541,7 +549,7 @@ struct ZwaveConfig {
     static constexpr int OYS = SHARE ? OWN : OY;                  // widest output rows of a CTA
     static constexpr int OYC = CY > 1 ? (PACE ? CY * OY : CY * OWN - 2 * (TB - 1) * R) : OY;
     static constexpr int OYE = SHARE ? LY - R - H : OY;           // outer CTAs' output rows
-    static constexpr int OXM = NARROW ? LXC : LX - 2 * H;  // widest output tile (x halo = H)
+    static constexpr int OXM = NARROW ? LXC - 2 * (TB - 1) * R : LX - 2 * H;  // widest output tile
     static constexpr int CELLS = LX * LY;
     static constexpr int CELLS_S = round16(CELLS);  // ring slot stride (TMA: 128-byte aligned)
     // threads cover the level-1 valid rows [R, LY - R) only: the R outermost rows of the
@@ -566,13 +574,13 @@ struct ZwaveConfig {
     static constexpr int NAR = NAUX > 0 ? (CQ ? 1 : (TB - 1) * R + 1) + PA : 0;  // aux ring depth
     static constexpr int AUXPLANE = NAUX * AYX;
     // guard rows before/after the rings: unconditional edge-cell stencils stay in bounds
-    static constexpr int GUARD = round16(LX * R + R + 8);
+    static constexpr int GUARD = NARROW ? 16 : round16(LX * R + R + 8);  // (NARROW stays in the box)
     static constexpr int STAGE = DOUT ? 0 : round16(OXM * OYS);  // one output staging plane
     static constexpr size_t SMEM_DOUBLES = size_t(GUARD) * 2 + size_t(NRING) * CELLS_S +
                                            size_t(NAR) * AUXPLANE + 3 * size_t(STAGE);
     static constexpr size_t SMEM = SMEM_DOUBLES * sizeof(double) + (NR0 + NAR) * sizeof(uint64_t);
     static_assert((CR * LXC) % (2 * NT) == 0, "computed rows must split evenly into cell pairs");
-    static_assert(!NARROW || (TB == 1 && CY == 1), "NARROW: single-step, non-cluster kernels");
+    static_assert(!NARROW || (CY == 1 && (TB == 1 || DOUT)), "NARROW: non-cluster kernels; fused ones store directly");
     static_assert(NT % 32 == 0, "whole warps");
     static_assert(!STACK || CR % (NT / 32) == 0, "STACK: every warp owns whole rows");
     static_assert(LXC % 32 == 0, "a warp must cover one tile row (warp-uniform row activity)");
@@ -733,7 +741,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
         }
         const int j = vcur.ug.za - H + vcur.it;
         const int slot = int(vnext % NR0);
-        const int xd = p.off + vcur.ug.tx * p.ox + R - p.hx;  // even by construction
+        const int xd = p.off + vcur.ug.tx * p.ox + p.xorg;  // even by construction
         const int yd = vcur.ug.ty * OYC + crank * OWN + R - H;
         mbar_arrive_expect_tx(&vbar[slot], PLANE_BYTES);
         tma_load_plane(ring0 + slot * CELLS_S, &cd.d[CHAIN ? cd.pidx[vcur.q] : 0].vmap, xd, yd, j,
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             if (acur.u >= total) return;
             const int k1 = acur.ug.za - H + acur.it - R;  // level-1 plane of that iteration
             const int slot = int(anext % NAR);
-            const int xd = p.off + acur.ug.tx * p.ox + R - p.hx + AXO;
+            const int xd = p.off + acur.ug.tx * p.ox + p.xorg + AXO;
             const int yd = acur.ug.ty * OYC + crank * OWN + R - H + AYO;
             if (acur.it < 2 * R) {
                 // no level reads the aux plane of the first 2R iterations of a unit: complete
@@ -843,6 +851,18 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     //      XA+1 aligned pair loads. Bit 2i+q of a mask = cell q of pair i. ----
     int lcell[PPT], dyv[PPT], ai[PPT], sidx[PPT];
     uint32_t out_mask = 0;
+    // box row / column of pair i's first cell, straight from the thread index (NARROW boxes
+    // are 68 or 72 columns wide: no division by LX in the per-unit mask setup)
+    auto cell_ly = [&](int i) -> int {
+        return CFG::STACK ? R + (tid >> 5) * PPT + i
+               : NARROW   ? R + 2 * (tid + NT * i) / LXC
+                          : (2 * (tid + NT * i) + R * LX) / LX;
+    };
+    auto cell_lx = [&](int i) -> int {
+        return CFG::STACK ? XO + 2 * (tid & 31)
+               : NARROW   ? XO + 2 * (tid + NT * i) % LXC
+                          : (2 * (tid + NT * i) + R * LX) % LX;
+    };
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
         // first cell of the pair (even)
@@ -850,7 +870,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                       : NARROW   ? (R + 2 * (tid + NT * i) / LXC) * LX + XO + 2 * (tid + NT * i) % LXC
                                  : 2 * (tid + NT * i) + R * LX;
         lcell[i] = c;
-        const int lx = c % LX, ly = c / LX;
+        const int lx = cell_lx(i), ly = cell_ly(i);
         // distance to the nearest box edge that has a trapezoid halo (inner cluster edges have
         // none: the neighbour supplies the rows beyond them)
         const int dy = min((CY > 1 && !lo_edge) ? 1 << 20 : ly,
@@ -931,7 +951,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             }
         }
         const int n_it = (ug.zb - ug.za) + 2 * H;
-        const int xa0 = ug.tx * p.ox + R - p.hx;  // allocated x of local lx = 0
+        const int xa0 = ug.tx * p.ox + p.xorg;  // allocated x of local lx = 0
         const int ya0 = ug.ty * OYC + crank * OWN + R - H;
 
         // ghost columns (ghost value instead of the stencil) and in-allocation columns
@@ -942,7 +962,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int b = 2 * i + q;
-                const int xa = xa0 + (lcell[i] + q) % LX, ya = ya0 + lcell[i] / LX;
+                const int xa = xa0 + cell_lx(i) + q, ya = ya0 + cell_ly(i);
                 if (xa >= 0 && xa < p.X && ya >= 0 && ya < p.Y) ok_mask |= 1u << b;
                 if (xa < R || xa >= R + p.nx || ya < R || ya >= R + p.ny) ghost_mask |= 1u << b;
                 // TMA stores clip x at 16-byte granularity, so the store map stops at an even
@@ -1325,7 +1345,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                                 for (int q = 0; q < 2; ++q) {
                                     const int b = 2 * i + q;
                                     if (!((out_mask >> b) & 1) || ((ghost_mask >> b) & 1)) continue;
-                                    const int xa = xa0 + (lcell[i] + q) % LX, ya = ya0 + lcell[i] / LX;
+                                    const int xa = xa0 + cell_lx(i) + q, ya = ya0 + cell_ly(i);
                                     const long long cell = ((long long)kz * p.ny + (ya - R)) * p.nx + (xa - R);
                                     for (int s2 = 0; s2 < TB; ++s2)
                                         atomicAdd(p.ledger + (long long)(p.ledger_t + s2) * p.nzg * p.ny * p.nx + cell, 1u);

@@ -98,9 +98,9 @@ def test_every_variant(girih, oracle, kind):
 
 
 def test_narrow_variants(girih, oracle):
-    # output-columns-only tiles (ZwaveConfig::NARROW): several 64-column tiles per row with a
-    # partial last one and odd extents, per-pass and chained launches, forced z chunks,
-    # emulated slabs and an odd start level
+    # inner-columns-only tiles (ZwaveConfig::NARROW): several tiles per row with a partial last
+    # one and odd extents, per-pass and chained launches, forced z chunks, emulated slabs and an
+    # odd start level
     g = girih
     vs = [v for v in g.variants() if v["narrow"]]
     assert vs, "no NARROW variant compiled"
@@ -110,9 +110,10 @@ def test_narrow_variants(girih, oracle):
         oracle.naive_sweep(base, 1)
         ref = base.copy()
         oracle.naive_sweep(ref, 5)
-        for cfg in (g.GpuConfig(tb=1, variant=v["index"], chain=-1),
-                    g.GpuConfig(tb=1, variant=v["index"], chain=1, zchunks=3),
-                    g.GpuConfig(tb=1, variant=v["index"], emulate_slabs=2)):
+        tb = v["tb"]  # fused narrow tiles start one column into the ghost cells (odd x halo)
+        for cfg in (g.GpuConfig(tb=tb, variant=v["index"], chain=-1),
+                    g.GpuConfig(tb=tb, variant=v["index"], chain=1, zchunks=3),
+                    g.GpuConfig(tb=tb, variant=v["index"], emulate_slabs=2)):
             st = to_problem(g, base)
             g.run(st, 5, cfg)
             assert_state_equal(st, ref, f"variant {v} cfg {cfg}")
