@@ -107,8 +107,9 @@ typedef struct {
     int direct_out;         /* 1: output stored from registers (no smem staging + TMA store) */
     int paced;              /* 1: cluster of independent y-neighbour tiles kept on the same z
                                plane by a per-plane cluster barrier (shared rows hit L2) */
-    int narrow;             /* x halo XO > 0: the threads compute only the lx - 2 XO output
-                               columns of the lx-wide box (single-step kernels); 0: all lx */
+    int narrow;             /* > 0: the threads compute only the inner columns of the lx-wide
+                               box, and this is the output tile's x halo (output tile width
+                               lx - 2 narrow); 0: threads on all lx columns */
 } girih_gpu_variant;
 
 const char* girih_gpu_last_error(void);
