@@ -49,9 +49,9 @@ def test_variants_registry(girih):
         assert v["smem_bytes"] <= 227 * 1024
         R = 1 if v["kind"] < 2 else 4
         # threads cover the level-1 rows [R, ly - R) in x-pairs
-        # threads cover all lx columns, or (narrow = the output tile's x halo) the inner ones
-            xo = v["narrow"] - (v["tb"] - 1) * R if v["narrow"] else 0
-            assert (v["lx"] - 2 * xo) * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
+        # (all lx columns, or the inner ones when narrow = the output tile's x halo is set)
+        xo = v["narrow"] - (v["tb"] - 1) * R if v["narrow"] else 0
+        assert (v["lx"] - 2 * xo) * (v["ly"] - 2 * R) % (2 * v["threads"]) == 0 and v["threads"] % 32 == 0
         assert v["lx"] > 2 * R * v["tb"]
         if v["cluster_y"] == 1:
             assert v["ly"] > 2 * R * v["tb"]
