@@ -219,7 +219,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifndef GIRIH_MBAR_HINT
+#define GIRIH_MBAR_HINT 0  // A/B: suspend-time hint (ns) of the TMA waits (0 = the default limit)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if GIRIH_MBAR_HINT > 0
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(uint32_t(GIRIH_MBAR_HINT))
+        : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -229,6 +243,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
