@@ -56,6 +56,9 @@
 #ifndef GIRIH_ZPS
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
 #endif
+#ifndef GIRIH_ZPS_ALL25
+#define GIRIH_ZPS_ALL25 0  // A/B: ZPS for single-pass const25pt without PHZ
+#endif
 #ifndef GIRIH_LOCK
 #define GIRIH_LOCK 0  // lockstep pacing compiled in (PassParams::lock; A/B builds only: its
                       // producer state cost the bench kernel a spill and 2-4%)
@@ -934,7 +937,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     // queue to fit the register budget (the 8-entry version spilled)
     constexpr bool PHZ = GIRIH_PHZ && TB == 1 &&
                          (GIRIH_PHZ_ALL ? R == 4 : (KIND == K_CONST25 && !CHAIN));
-    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && ((KIND == K_CONST25 && CHAIN) || PHZ);
+    constexpr bool ZPS = GIRIH_ZPS && TB == 1 && ((KIND == K_CONST25 && (CHAIN || GIRIH_ZPS_ALL25)) || PHZ);
     constexpr int ZQD = ZPS ? R : 2 * R;
     double2 zq[TB][PPT][ZQD];
 #pragma unroll
