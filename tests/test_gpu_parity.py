@@ -119,6 +119,29 @@ def test_narrow_variants(girih, oracle):
             assert_state_equal(st, ref, f"variant {v} cfg {cfg}")
 
 
+def test_narrow_tile_boundaries(girih, oracle):
+    # inner-columns-only tiles at the extents where their tile count changes: multiples of the
+    # output tile width (64, or 62 for the fused var7pt tile whose grid starts on the ghost
+    # column) and one column either side, with and without row padding
+    g = girih
+    for v in [v for v in g.variants() if v["narrow"]]:
+        kind, tb = v["kind"], v["tb"]
+        R = 1 if kind < 2 else 4
+        ox = v["lx"] - 2 * v["narrow"]
+        shift = 1 if tb > 1 else 0  # first output column of the grid is a ghost column
+        for nx in sorted({ox - shift - 1, ox - shift, ox - shift + 1, 2 * ox - shift, 2 * ox - shift + 1}):
+            if nx < 2 * R + 1:
+                continue
+            pad = nx % 3
+            base = oracle.init_state(kind, nx, 2 * R + 5, 2 * R + 3, pad, 1000 + nx, remap=True)
+            steps = 2 * tb + 1
+            ref = base.copy()
+            oracle.naive_sweep(ref, steps)
+            st = to_problem(g, base)
+            g.run(st, steps, g.GpuConfig(tb=tb, variant=v["index"]))
+            assert_state_equal(st, ref, f"variant {v['index']} nx={nx} pad={pad}")
+
+
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_cluster_variants(girih, oracle, kind):
     # thread-block clusters along y (the fused levels' halo rows shared through distributed
