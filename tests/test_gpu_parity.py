@@ -534,12 +534,15 @@ def test_randomised_configurations(girih, oracle):
     # seeded fuzz over the configuration space the fixed cases do not enumerate: extents, pad,
     # start level, step count, fused depth, variant, z chunks, emulated slabs, drop-in vs
     # device-resident handle -- every result bitwise equal to the oracle, ghosts and pad included
+    # (soak runs: GIRIH_FUZZ_SEED / GIRIH_FUZZ_CASES choose another stream and length,
+    # GIRIH_FUZZ_WIDE=1 draws nx up to 200 so that several tile columns take part)
     g = girih
-    rng = np.random.default_rng(20261020)
+    rng = np.random.default_rng(int(os.environ.get("GIRIH_FUZZ_SEED", "20261020")))
+    wide = os.environ.get("GIRIH_FUZZ_WIDE", "0") == "1"
     by_kind = {}
     for v in g.variants():
         by_kind.setdefault(v["kind"], []).append(v)
-    for case in range(150):
+    for case in range(int(os.environ.get("GIRIH_FUZZ_CASES", "150"))):
         kind = int(rng.integers(0, 4))
         R = 1 if kind < 2 else 4
         vs = by_kind[kind]
@@ -547,6 +550,8 @@ def test_randomised_configurations(girih, oracle):
         tb = v["tb"]
         lo = 2 * R + 1
         nx, ny = (int(rng.integers(lo, lo + 45)) for _ in range(2))
+        if wide:
+            nx = int(rng.integers(lo, 200))
         nz = int(rng.integers(lo, lo + 40)) if rng.random() < 0.8 else int(rng.integers(64, 90))
         pad = int(rng.integers(0, 4))
         t0 = int(rng.integers(0, 3))
@@ -559,9 +564,10 @@ def test_randomised_configurations(girih, oracle):
             oracle.naive_sweep(base, t0)
         ref = base.copy()
         oracle.naive_sweep(ref, steps)
-        cfg = g.GpuConfig(tb=tb, variant=v["index"], zchunks=zc, emulate_slabs=slabs)
+        chain = int(rng.choice([0, 1, -1])) if (wide and slabs == 0 and v["cluster_y"] == 1) else 0
+        cfg = g.GpuConfig(tb=tb, variant=v["index"], zchunks=zc, emulate_slabs=slabs, chain=chain)
         what = (f"case {case}: {KIND_IDS[kind]} {nx}x{ny}x{nz}+{pad} t0={t0} T={steps} tb={tb} "
-                f"variant={v['index']} zc={zc} slabs={slabs}")
+                f"variant={v['index']} zc={zc} slabs={slabs} chain={chain}")
         if rng.random() < 0.5:
             st = to_problem(g, base)
             g.run(st, steps, cfg)
