@@ -249,6 +249,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
+// the same on a precomputed shared-window address (no generic-to-shared conversion per wait)
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar_s, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar_s),
+        "r"(phase)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n"
@@ -949,6 +962,21 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
 
     __syncthreads();  // uq[0] visible
     uint32_t g = G0;  // consumer's global element index
+    // g's ring slots and mbarrier phase parities, advanced with g instead of recomputed every
+    // iteration by divisions by the ring depths (6 and 2-3 planes: not powers of two); G0 is a
+    // multiple of 2 NR0 and 2 NAR, so both start at slot 0, parity 0
+    int gs = 0, as = 0;
+    uint32_t gph = 0, aph = 0;
+    const uint32_t vbar_s = smem_u32(vbar), abar_s = smem_u32(abar);
+    // slot of the plane `back` iterations before g's
+    auto vslot = [&](int back) -> int {
+        const int sl = gs - back % NR0;
+        return sl < 0 ? sl + NR0 : sl;
+    };
+    auto aslot = [&](int back) -> int {
+        const int sl = as - back % (NAR > 0 ? NAR : 1);
+        return sl < 0 ? sl + NAR : sl;
+    };
     unsigned long long unit_t0 = 0;  // instrumentation: start of thread 0's current unit
     for (int seq = 0;; ++seq) {
         const int u = reinterpret_cast<volatile int*>(uq)[seq % UQ];
@@ -992,6 +1020,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 colidx[b] = cy * p.pitch + p.off + cx;
             }
         const uint32_t col_fix = ghost_mask & ok_mask;
+        const uint32_t dmask = out_mask & ~ghost_mask;  // cells this thread stores (direct output)
         const bool any_ghost_col = __syncthreads_or(col_fix != 0);
         const bool any_odd_col = (p.nx & 1) && ug.tx == p.tiles_x - 1;  // owner of the last column
 
@@ -1072,20 +1101,20 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                     if ((fix >> (2 * i + 1)) & 1) gh[s - 1][i].y = __ldg(ghost + colidx[2 * i + 1]);
                 }
             }
-            mbar_wait(&vbar[g % NR0], (g / NR0) & 1);
-            if constexpr (NAUX > 0) mbar_wait(&abar[g % NAR], (g / NAR) & 1);
+            mbar_wait_s(vbar_s + 8u * uint32_t(gs), gph);
+            if constexpr (NAUX > 0) mbar_wait_s(abar_s + 8u * uint32_t(as), aph);
             if (tr) trp[1] = clock64();
 
             // level-0 newest plane j into the level-0 z queue input (one LDS.128 per pair)
             double2 newest[PPT];  // level s-1 at (pair, k_s + R), produced this iteration
             {
-                const double2* pj = reinterpret_cast<const double2*>(ring0 + (g % NR0) * CELLS_S);
+                const double2* pj = reinterpret_cast<const double2*>(ring0 + gs * CELLS_S);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) newest[i] = pj[lcell[i] >> 1];
             }
             double2 ctrk[ZPS ? PPT : 1];  // ZPS: level 0 at the centre plane k = j - R
             if constexpr (ZPS) {
-                const double2* pk = reinterpret_cast<const double2*>(ring0 + ((g - R) % NR0) * CELLS_S);
+                const double2* pk = reinterpret_cast<const double2*>(ring0 + vslot(R) * CELLS_S);
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) ctrk[i] = pk[lcell[i] >> 1];
             }
@@ -1124,10 +1153,10 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                 const bool plane_ghost = kg < R || kg >= R + p.nzg;
                 // centre plane k of level s-1 (x/y neighbours, other threads' values)
                 const double2* pc = reinterpret_cast<const double2*>(
-                    s == 1 ? ring0 + ((g - R) % NR0) * CELLS_S
+                    s == 1 ? ring0 + vslot(R) * CELLS_S
                            : ringL + ((s - 2) * QL + (k + KOFF) % QL) * CELLS_S);
                 const double2* aux = NAUX > 0 ? reinterpret_cast<const double2*>(
-                                                    auxr + ((g - (s - 1) * R) % NAR) * AUXPLANE)
+                                                    auxr + aslot((s - 1) * R) * AUXPLANE)
                                               : nullptr;
 
                 // (1) stencil for every pair of the valid rows; cells outside the valid area in x
@@ -1195,7 +1224,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         if (dz == R) return newest[i];
                         if (ZPS && dz > 0)
                             return reinterpret_cast<const double2*>(
-                                ring0 + ((g - R + dz) % NR0) * CELLS_S)[lcell[i] >> 1];
+                                ring0 + vslot(R - dz) * CELLS_S)[lcell[i] >> 1];
                         return zq[s - 1][i][(dz + R + PH) % ZQD];
                     };
                     auto Cp = [&](int a) -> double2 { return aux[(a * AYX + ai[i]) >> 1]; };
@@ -1315,14 +1344,21 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         // map's clipping, done by the masks); a full pair is one aligned
                         // 16-byte store (x pair origins are even, off + R is even)
                         double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
+                        constexpr uint32_t FULL = PPT == 16 ? 0xffffffffu : (1u << (2 * PPT)) - 1u;
+                        if (dmask == FULL) {  // every pair whole (all threads of interior tiles)
 #pragma unroll
-                        for (int i = 0; i < PPT; ++i) {
-                            const uint32_t m = ((out_mask & ~ghost_mask) >> (2 * i)) & 3u;
-                            if (m == 3u) {
+                            for (int i = 0; i < PPT; ++i)
                                 *reinterpret_cast<double2*>(dst + colidx[2 * i]) = val[i];
-                            } else {
-                                if (m & 1u) dst[colidx[2 * i]] = val[i].x;
-                                if (m & 2u) dst[colidx[2 * i + 1]] = val[i].y;
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < PPT; ++i) {
+                                const uint32_t m = (dmask >> (2 * i)) & 3u;
+                                if (m == 3u) {
+                                    *reinterpret_cast<double2*>(dst + colidx[2 * i]) = val[i];
+                                } else {
+                                    if (m & 1u) dst[colidx[2 * i]] = val[i].x;
+                                    if (m & 2u) dst[colidx[2 * i + 1]] = val[i].y;
+                                }
                             }
                         }
                     } else {
@@ -1370,7 +1406,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                                 }
                         }
                     }
-                    if constexpr (!CHAIN) {
+                    if (!CHAIN && p.push_hz > 0) {  // (push_hz = 0: no neighbour slabs)
                         // halo push: boundary planes go to the neighbour slab as they are made
                         const bool dn = p.push_dn_final && k < p.zout_lo + p.push_hz;
                         const bool up = p.push_up_final && k >= p.zout_hi - p.push_hz;
@@ -1505,6 +1541,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             }
             if (tr) trp[3] = clock64();
             ++g;
+            if (++gs == NR0) {
+                gs = 0;
+                gph ^= 1u;
+            }
+            if constexpr (NAR > 0) {
+                if (++as == NAR) {
+                    as = 0;
+                    aph ^= 1u;
+                }
+            }
         };
         constexpr int NPH = PHZ ? ZQD : 1;
         for (int it0 = 0; it0 < n_it; it0 += NPH) {
