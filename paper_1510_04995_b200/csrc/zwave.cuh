@@ -1346,9 +1346,18 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
                         constexpr uint32_t FULL = PPT == 16 ? 0xffffffffu : (1u << (2 * PPT)) - 1u;
                         if (dmask == FULL) {  // every pair whole (all threads of interior tiles)
+                            if constexpr (CFG::STACK) {
+                                // a thread's pairs sit in consecutive rows of one column (no
+                                // clamped coordinate in a whole-pair thread): one base, row pitch
+                                double* d0 = dst + colidx[0];
 #pragma unroll
-                            for (int i = 0; i < PPT; ++i)
-                                *reinterpret_cast<double2*>(dst + colidx[2 * i]) = val[i];
+                                for (int i = 0; i < PPT; ++i)
+                                    *reinterpret_cast<double2*>(d0 + i * p.pitch) = val[i];
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < PPT; ++i)
+                                    *reinterpret_cast<double2*>(dst + colidx[2 * i]) = val[i];
+                            }
                         } else {
 #pragma unroll
                             for (int i = 0; i < PPT; ++i) {
