@@ -56,6 +56,9 @@
 #ifndef GIRIH_ZPS
 #define GIRIH_ZPS 1  // single-step radius-4 passes: z+ neighbours from the level-0 ring
 #endif
+#ifndef GIRIH_PHQ
+#define GIRIH_PHQ 0  // A/B: single-pass var7pt TB = 2 rotates its z and coefficient queues by renaming (PHQ: -13%)
+#endif
 #ifndef GIRIH_ZPS_ALL25
 #define GIRIH_ZPS_ALL25 0  // A/B: ZPS for single-pass const25pt without PHZ
 #endif
@@ -937,8 +940,15 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     __shared__ UnitState SU2[2];
     const bool has_penult_1 = p.dst_penult != nullptr;  // single-pass launches
     // coefficient queue (CQ): cq[L][pair] = coefficients level 1 used L+1 iterations ago
+    // PHQ (single-pass var7pt TB = 2, A/B builds): the 2-entry z queues and the coefficient queue
+    // rotate by renaming over 2 unrolled iteration phases (level 1 fills one of two coefficient
+    // register sets, level 2 reads the other) instead of being shifted (the shifts are 44 of
+    // the kernel's 282 instructions per warp and plane). Measured: the two-phase body spills
+    // 48 B at the 128-register cap and runs 13% slower (122.5 K vs 141.6 K at 1024^3)
+    constexpr bool PHQ = GIRIH_PHQ && CQ && TB == 2 && R == 1 && !CHAIN && CY == 1;
     constexpr int CQD = CQ ? TB - 1 : 1, CQN = CQ ? 7 : 1;
     double2 cq[CQD][PPT][CQN], cnew[PPT][CQN];
+    double2 cqr[PHQ ? 2 : 1][PPT][CQN];  // PHQ: the two coefficient sets (phase parity)
     // per-thread z queues: zq[L][pair][d] = level L at plane (newest_L - 2R + d), d = 0..2R-1
     // ZPS (single-step radius-4 passes): the z+ neighbours k+1..k+R-1 are read from the level-0
     // ring, which holds planes k..k+R anyway, so the queue keeps only k-R..k-1 (fewer registers;
@@ -948,8 +958,8 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
     // PHZ (single-pass const25pt): the 4-entry z- queue rotates by renaming over 4 unrolled
     // iteration phases instead of 64 register moves per warp-iteration; it needs ZPS's short
     // queue to fit the register budget (the 8-entry version spilled)
-    constexpr bool PHZ = GIRIH_PHZ && TB == 1 &&
-                         (GIRIH_PHZ_ALL ? R == 4 : (KIND == K_CONST25 && !CHAIN));
+    constexpr bool PHZ = (GIRIH_PHZ && TB == 1 &&
+                          (GIRIH_PHZ_ALL ? R == 4 : (KIND == K_CONST25 && !CHAIN))) || PHQ;
     constexpr bool ZPS = GIRIH_ZPS && TB == 1 && ((KIND == K_CONST25 && (CHAIN || GIRIH_ZPS_ALL25)) || PHZ);
     constexpr int ZQD = ZPS ? R : 2 * R;
     double2 zq[TB][PPT][ZQD];
@@ -1247,10 +1257,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         if (!CQ || s == 1) {
 #pragma unroll
                             for (int a = 0; a < 7; ++a) cf[a] = Cp(a);
-                            if constexpr (CQ) {
+                            if constexpr (PHQ) {
+#pragma unroll
+                                for (int a = 0; a < 7; ++a) cqr[PHQ ? PH & 1 : 0][i][CQ ? a : 0] = cf[a];
+                            } else if constexpr (CQ) {
 #pragma unroll
                                 for (int a = 0; a < 7; ++a) cnew[i][a] = cf[a];
                             }
+                        } else if constexpr (PHQ) {  // the set level 1 filled one iteration ago
+#pragma unroll
+                            for (int a = 0; a < 7; ++a) cf[a] = cqr[PHQ ? (PH + 1) & 1 : 0][i][CQ ? a : 0];
                         } else {
 #pragma unroll
                             for (int a = 0; a < 7; ++a) cf[a] = cq[CQ ? s - 2 : 0][i][CQ ? a : 0];
@@ -1485,7 +1501,7 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
             if constexpr (CSYNC)
                 cluster_arrive();  // this iteration's ring rows are complete
             // advance every level's z queue by one plane (and the coefficient queue)
-            if constexpr (CQ) {
+            if constexpr (CQ && !PHQ) {
 #pragma unroll
                 for (int L = CQD - 1; L > 0; --L)
 #pragma unroll
