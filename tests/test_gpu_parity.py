@@ -209,6 +209,25 @@ def test_instrumented_run_ledger_and_trace(girih, oracle, kind):
         assert (order == np.arange(len(trace))).all()
 
 
+def test_instrumented_run_narrow_variants(girih, oracle):
+    # the exactly-once ledger and the trace through the inner-columns-only tiles, with several
+    # tile columns (the fused var7pt tile's grid starts on the ghost column: its first output
+    # column must not be counted, its last tile column must be)
+    g = girih
+    for v in [v for v in g.variants() if v["narrow"]]:
+        kind = v["kind"]
+        nx, ny, nz, T = 131, 23, 13, 2 * v["tb"] + 1
+        base = oracle.init_state(kind, nx, ny, nz, 1, 5, remap=True)
+        ref = base.copy()
+        oracle.naive_sweep(ref, T)
+        st = to_problem(g, base)
+        cfg = g.GpuConfig(tb=v["tb"], variant=v["index"])
+        rep, trace, led = g.run_instrumented(st, T, cfg)
+        assert_state_equal(st, ref, f"instrumented narrow {v['index']}")
+        assert led.shape == (T, nz, ny, nx) and (led == 1).all(), f"ledger {v['index']}: {np.unique(led)}"
+        assert len(trace) == rep.units > 0
+
+
 @pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
 def test_update_units_piecewise_passes(girih, oracle, kind):
     # update_tile counterpart: each pass of a plan run as shuffled pieces of its work units (any
