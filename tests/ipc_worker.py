@@ -20,11 +20,16 @@ def main():
     bad = 0
     # (the last two: slabs of several z-chunk rows, so boundary rows run first and interior
     # rows overlap the neighbours' next pass; the kernel signals the neighbours)
-    for kind, (nx, ny, nz), steps, zc in ((1, (40, 33, 50), 9, 0), (3, (37, 30, 52), 5, 0),
-                                          (2, (36, 29, 48), 6, 0), (0, (41, 35, 47), 7, 0),
-                                          (1, (70, 45, 150), 7, 6), (3, (45, 38, 160), 4, 7)):
+    # (the last two again: the inner-columns-only tiles forced on grids of several tile columns;
+    # the fused var7pt one starts its tile grid on the ghost column)
+    narrow = {k: next(v for v in g.variants() if v["kind"] == k and v["narrow"]) for k in (0, 1)}
+    for kind, (nx, ny, nz), steps, zc, var in ((1, (40, 33, 50), 9, 0, None), (3, (37, 30, 52), 5, 0, None),
+                                               (2, (36, 29, 48), 6, 0, None), (0, (41, 35, 47), 7, 0, None),
+                                               (1, (70, 45, 150), 7, 6, None), (3, (45, 38, 160), 4, 7, None),
+                                               (1, (131, 30, 60), 7, 0, narrow[1]), (0, (131, 30, 60), 5, 0, narrow[0])):
         grid = g.GridSpec(nx, ny, nz, 0)
-        cfg = g.GpuConfig(device=dev, zchunks=zc)
+        cfg = (g.GpuConfig(device=dev, zchunks=zc) if var is None else
+               g.GpuConfig(device=dev, zchunks=zc, tb=var["tb"], variant=var["index"]))
         with g.DeviceState.slab_seeded(kind, grid, 17, True, rank, world, None, cfg) as ds:
             blobs = [None] * world
             dist.all_gather_object(blobs, ds.ipc_export())
