@@ -1774,7 +1774,8 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             // vs 139.4-140.9 K MLUP/s, same box); 13-16 columns (768, 960): +-0.5%, row-major stays
             const int strip = lk.strip >= 0 ? lk.strip
                               : (h.kind == K_VAR7 && ps.tb == 2 && p.tiles_x >= 17) ? 8 : 0;
-            if (strip > 0 && !h.instr.on && !ipc_flags) p.ustrip = strip;
+            // (IPC slabs too: the boundary-rows-first remap acts on the z-chunk row of either order)
+            if (strip > 0 && !h.instr.on) p.ustrip = strip;
             if (lk.blk > 0 && var->cy == 1 && !h.instr.on && p.units > li.grid && !ipc_flags) {
                 if (lock_base[g] > (1ull << 62)) {
                     GCHECK(cudaMemsetAsync(reinterpret_cast<char*>(s.work->p) + 8, 0, 8, s.stream));

@@ -387,19 +387,20 @@ __device__ __forceinline__ UnitGeom unit_geom(const PassParams& p, int u) {
         const int tile = grp * p.ugroup + (w - zc * gsz);
         g.tx = tile % p.tiles_x;
         g.ty = tile / p.tiles_x;
-    } else if (GIRIH_UORDER && p.ustrip > 0) {
+    } else {
         const int txy = p.tiles_x * p.tiles_y;
         zc = u / txy;
-        const int tile = u - zc * txy, sw = p.ustrip * p.tiles_y;  // tiles per full strip
-        const int strip = tile / sw, w = min(p.ustrip, p.tiles_x - strip * p.ustrip);
-        const int r = tile - strip * sw;
-        g.ty = r / w;
-        g.tx = strip * p.ustrip + (r - g.ty * w);
-    } else {
-        g.tx = u % p.tiles_x;
-        const int r = u / p.tiles_x;
-        g.ty = r % p.tiles_y;
-        zc = r / p.tiles_y;
+        const int tile = u - zc * txy;
+        if (GIRIH_UORDER && p.ustrip > 0) {
+            const int sw = p.ustrip * p.tiles_y;  // tiles per full strip
+            const int strip = tile / sw, w = min(p.ustrip, p.tiles_x - strip * p.ustrip);
+            const int r = tile - strip * sw;
+            g.ty = r / w;
+            g.tx = strip * p.ustrip + (r - g.ty * w);
+        } else {
+            g.ty = tile / p.tiles_x;
+            g.tx = tile - g.ty * p.tiles_x;
+        }
         if (p.zb_lo + p.zb_hi > 0) {  // boundary rows first: bottom rows, top rows, interior
             if (zc >= p.zb_lo) zc = zc < p.zb_lo + p.zb_hi ? p.nzc - p.zb_hi + (zc - p.zb_lo)
                                                            : zc - p.zb_hi;
