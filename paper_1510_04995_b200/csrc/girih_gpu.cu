@@ -190,9 +190,14 @@ const Variant* select_chain_variant(int kind, int tb, int requested) {
 // the ghost column) needs fewer tile columns than the 60-column one, it is the default (1024:
 // 17 instead of 18; same box, fresh processes: 138.6 K vs 137.0 K MLUP/s, DRAM reads 85.5 vs
 // 87.5 GB per pass); elsewhere it is equal or up to 1% slower (512^3: 134.6 K vs 136.2 K).
-const Variant* default_variant(int kind, int tb, int nx) {
+// Planes below ~560^2 cells take the same 64x18 tile with a 1-plane coefficient prefetch instead
+// of 2 (same box, fresh processes, final build: 320^3 132.6 K vs 127.6 K, 384^3 142.0 K vs 130.5 K,
+// 448^3 140.5 K vs 136.8 K, 512^3 141.3 K vs 138.4 K; 256^3 and 576^3 equal; 640^3 and up the
+// deeper prefetch wins by 1-2%).
+const Variant* default_variant(int kind, int tb, int nx, long long plane_cells) {
     int n;
     const Variant* t = variant_table(kind, &n);
+    const int var7_pa = plane_cells < 560ll * 560 ? 1 : 2;
     if (kind == K_VAR7 && tb == 2 && (nx + 1 + 61) / 62 < (nx + 59) / 60) {
         for (int i = 0; i < n; ++i)
             if (t[i].tb == 2 && t[i].narrow && t[i].lx == 68 && t[i].ly == 18 &&
@@ -201,7 +206,8 @@ const Variant* default_variant(int kind, int tb, int nx) {
     }
     for (int i = 0; i < n; ++i) {
         if (t[i].tb != tb || !t[i].direct_out || t[i].cy != 1 || t[i].narrow) continue;
-        if (kind == K_VAR7 && tb == 2 && t[i].lx == 64 && t[i].ly == 18 && t[i].aux_prefetch == 2)
+        if (kind == K_VAR7 && tb == 2 && t[i].lx == 64 && t[i].ly == 18 &&
+            t[i].aux_prefetch == var7_pa)
             return &t[i];
         if (kind == K_CONST7 && tb == 1 && t[i].lx == 64 && t[i].ly == 10) return &t[i];
     }
@@ -1530,7 +1536,7 @@ const Variant* pass_variant(const Handle& h, int tb) {
         const Variant* v = select_variant(h.kind, tb, h.cfg.variant);
         if (v->tb == tb) return v;
     }
-    return default_variant(h.kind, tb, h.nx);
+    return default_variant(h.kind, tb, h.nx, (long long)h.nx * h.ny);
 }
 
 StepStats do_step(Handle& h, long long steps, bool time_passes) {
