@@ -25,6 +25,10 @@
 //   * the tile shrinks by R per side per level (overlapped / trapezoid tiling in x and y,
 //     and in z at z-chunk boundaries), so no inter-CTA synchronisation exists inside a pass;
 //     the x halo is H or H+1 so that every TMA box starts on a 16-byte boundary;
+//   * inner-columns-only tiles (ZwaveConfig::NARROW): the box is 64 + 2 XO columns wide and the
+//     threads sit on its inner 64 columns, so a single-step tile outputs all 64 thread columns
+//     (tiles divide 256 / 512 exactly, no thread computes a halo column) and the fused var7pt
+//     tile 62 instead of 60;
 //   * work units (tile, z-chunk) are drawn dynamically in z-chunk-major order, which keeps
 //     neighbouring tiles within about a chunk of each other in z so shared halo rows are
 //     still in L2.
