@@ -324,7 +324,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
             # refuses it): rank 0 tunes a single-GPU handle of one slab's size and every rank
             # takes that configuration (broadcast), so all ranks run the same pass sequence
             import torch
-            vec = torch.zeros(4, dtype=torch.float64, device=tdev)
+            vec = torch.zeros(5, dtype=torch.float64, device=tdev)
             ml, nmeas = 0.0, 0
             if rank == 0:
                 sgrid = g.GridSpec(n, n, max(2 * (4 if kind >= 2 else 1) + 1, n // world))
@@ -333,10 +333,12 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
                     tcfg, ml, nmeas = tds.tune(max_tb=args.tb if args.tb > 0 else 0)
                 g.trim()
                 vec[0], vec[1], vec[2], vec[3] = tcfg.tb, tcfg.variant, tcfg.zchunks, tcfg.chain
+                vec[4] = tcfg.tile_order
             dist.broadcast(vec, 0)
-            tb_, var_, zc_, ch_ = (int(x) for x in vec.cpu().tolist())
-            ds.set_config(g.GpuConfig(tb=tb_, variant=var_, zchunks=zc_, chain=ch_, device=dev))
-            tuned = {"tb": tb_, "variant": var_, "zchunks": zc_, "chain": ch_,
+            tb_, var_, zc_, ch_, to_ = (int(x) for x in vec.cpu().tolist())
+            ds.set_config(g.GpuConfig(tb=tb_, variant=var_, zchunks=zc_, chain=ch_, device=dev,
+                                      tile_order=to_))
+            tuned = {"tb": tb_, "variant": var_, "zchunks": zc_, "chain": ch_, "tile_order": to_,
                      "tuned_on": f"rank 0, single-GPU {n}x{n}x{n // world} (one slab), broadcast",
                      "mlups": ml if rank == 0 else None, "measured": nmeas}
         else:
@@ -344,7 +346,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int):
             tcfg.device = dev
             ds.set_config(tcfg)
             tuned = {"tb": tcfg.tb, "variant": tcfg.variant, "zchunks": tcfg.zchunks,
-                     "chain": tcfg.chain, "mlups": tml, "measured": nmeas}
+                     "chain": tcfg.chain, "tile_order": tcfg.tile_order, "mlups": tml,
+                     "measured": nmeas}
     for _ in range(args.warmup):
         ds.step(T)
     if dist is not None:

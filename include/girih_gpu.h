@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define GIRIH_GPU_ABI_VERSION 5
+#define GIRIH_GPU_ABI_VERSION 6
 
 #define GIRIH_OK 0
 #define GIRIH_EINVAL (-1)
@@ -72,6 +72,10 @@ typedef struct {
                       work units start as soon as their neighbourhood finished the previous pass
                       (single-slab handles); -1 = one launch per pass; 0 = auto (chained for
                       grids of at most 256^3 cells, except var7pt) */
+    int tile_order;/* order of the tiles inside a z-chunk row of one-launch-per-pass runs: W > 0 =
+                      column strips of W tiles (y fastest inside a strip, so y-neighbour tiles are
+                      drawn W apart and share halo rows through L2); -1 = row-major; 0 = auto
+                      (strips of 8 for var7pt two-step passes on grids of >= 17 tile columns) */
 } girih_gpu_config;
 
 typedef struct {

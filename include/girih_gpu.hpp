@@ -35,6 +35,7 @@ struct GpuConfig {
     int graphs = 0;
     int chain = 0;     // 1 = chain same-depth passes into one dependency-driven launch; -1 = off;
                        // 0 = auto (small grids)
+    int tile_order = 0;  // W > 0 = column strips of W tiles per z-chunk row; -1 = row-major; 0 = auto
 };
 
 // PerfReport (engine.hpp:93-98) plus the GPU-side timings.
@@ -62,6 +63,7 @@ inline girih_gpu_config to_c(const GpuConfig& c) {
     o.device = c.device;
     o.graphs = c.graphs;
     o.chain = c.chain;
+    o.tile_order = c.tile_order;
     return o;
 }
 

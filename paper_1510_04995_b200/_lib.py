@@ -40,7 +40,7 @@ class GirihGpuConfig(C.Structure):
     _fields_ = [
         ("tb", C.c_int), ("variant", C.c_int), ("zchunks", C.c_int), ("ngpus", C.c_int),
         ("exact", C.c_int), ("device", C.c_int), ("graphs", C.c_int), ("reserved", C.c_int),
-        ("chain", C.c_int),
+        ("chain", C.c_int), ("tile_order", C.c_int),
     ]
 
 

@@ -588,7 +588,7 @@ struct Handle {
     std::vector<std::unique_ptr<MapEntry>> maps;
     struct GraphEntry {
         long long parity = 0, steps = 0;
-        int tb = 0, variant = 0, zchunks = 0, chain = 0;
+        int tb = 0, variant = 0, zchunks = 0, chain = 0, tile_order = 0;
         bool timed = false;
         cudaGraphExec_t exec = nullptr;
         StepStats st;
@@ -719,6 +719,7 @@ void validate_config(const girih_gpu_config& c, int kind) {
     if (c.tb < 0 || c.tb > max_tb(kind)) throw_err(GIRIH_EINVAL, "fused step count out of range");
     if (c.ngpus < 1) throw_err(GIRIH_EINVAL, "ngpus must be >= 1");
     if (c.zchunks < 0) throw_err(GIRIH_EINVAL, "zchunks must be >= 0");
+    if (c.tile_order < -1) throw_err(GIRIH_EINVAL, "tile_order must be >= -1");
     if (c.variant >= 0) {
         const Variant* v = variant_by_global(c.variant);
         if (!v || v->kind != kind) throw_err(GIRIH_EINVAL, "variant index does not match kind");
@@ -1270,6 +1271,12 @@ TileGeom tile_geom(const Handle& h, int tb, const Variant* var, int nzl, int max
     return t;
 }
 
+// cfg.tile_order = 0: column strips of 8 tiles for var7pt two-step passes on grids of at least 17
+// tile columns, row-major otherwise (measurements at the use in do_step)
+int auto_tile_strip(int kind, int tb, int tiles_x) {
+    return (kind == K_VAR7 && tb == 2 && tiles_x >= 17) ? 8 : 0;
+}
+
 // Lockstep pacing of single-pass launches (PassParams::lock) and the group-major unit order
 // that goes with it. GIRIH_LOCK_B = iterations per block (0 = off), GIRIH_LOCK_S = slack in
 // blocks, GIRIH_UGROUP = 0 keeps the z-chunk-major order (A/B switches).
@@ -1595,7 +1602,8 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         for (auto& e : h.graphs)
             if (e.parity == parity_of(h.t_current) && e.steps == steps && e.tb == tb &&
                 e.variant == h.cfg.variant && e.zchunks == h.cfg.zchunks &&
-                e.chain == h.cfg.chain && e.timed == time_passes)
+                e.chain == h.cfg.chain && e.tile_order == h.cfg.tile_order &&
+                e.timed == time_passes)
                 ge = &e;
         if (ge) {
             GCHECK(cudaSetDevice(h.slabs[0].device));
@@ -1778,8 +1786,11 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
             // at least 17 tile columns (1024: y-neighbour tiles start 8 draws apart instead of 17
             // and share their halo rows through L2: DRAM reads 81.1 vs 85.6 GB per pass, 143.3-144.7 K
             // vs 139.4-140.9 K MLUP/s, same box); 13-16 columns (768, 960): +-0.5%, row-major stays
-            const int strip = lk.strip >= 0 ? lk.strip
-                              : (h.kind == K_VAR7 && ps.tb == 2 && p.tiles_x >= 17) ? 8 : 0;
+            // (cfg.tile_order: W > 0 strips of W, -1 row-major, 0 this rule; GIRIH_USTRIP overrides)
+            const int strip = lk.strip >= 0         ? lk.strip
+                              : h.cfg.tile_order > 0 ? h.cfg.tile_order
+                              : h.cfg.tile_order < 0 ? 0
+                                                     : auto_tile_strip(h.kind, ps.tb, p.tiles_x);
             // (IPC slabs too: the boundary-rows-first remap acts on the z-chunk row of either order)
             if (strip > 0 && !h.instr.on) p.ustrip = strip;
             if (lk.blk > 0 && var->cy == 1 && !h.instr.on && p.units > li.grid && !ipc_flags) {
@@ -1857,6 +1868,7 @@ StepStats do_step(Handle& h, long long steps, bool time_passes) {
         e.variant = h.cfg.variant;
         e.zchunks = h.cfg.zchunks;
         e.chain = h.cfg.chain;
+        e.tile_order = h.cfg.tile_order;
         e.timed = time_passes;
         e.st = st;
         const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
@@ -3201,18 +3213,25 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         const int copts[] = {-1, 1};
         const int nc_opts = (h.slabs.size() == 1 && h.nranks == 1) ? 2 : 1;
         const int def_c = def_chain ? 1 : 0;  // index into copts of the default's scheduling
-        std::map<std::array<int, 3>, double> seen;
+        // tile order inside a z-chunk row (one launch per pass only): row-major, the auto rule,
+        // column strips of 4 or 8 tiles; the search starts at the auto rule
+        const int sopts[] = {-1, 0, 4, 8};
+        const int ns_opts = int(sizeof(sopts) / sizeof(sopts[0]));
+        const int def_s = 1;
+        std::map<std::array<int, 4>, double> seen;
         // adaptive_measure (tuner.cpp:47-71): double the test size until two runs agree
-        auto measure = [&](int vi, int zi, int ci) -> double {
-            const std::array<int, 3> key{vi, zi, ci};
+        auto measure = [&](int vi, int zi, int ci, int si) -> double {
+            const std::array<int, 4> key{vi, zi, ci, si};
             if (auto it = seen.find(key); it != seen.end()) return it->second;
             const Variant* v = variant_by_global(vars[vi]);
             if (copts[ci] > 0 && v->cy > 1) return 0.0;  // cluster tiles do not chain
+            if (copts[ci] > 0 && si != def_s) return 0.0;  // chained launches draw pass-major
             girih_gpu_config c = cfg_saved;
             c.tb = v->tb;
             c.variant = vars[vi];
             c.zchunks = zopts[zi];
             c.chain = copts[ci];
+            c.tile_order = sopts[si];
             h.cfg = c;
             // equal starting lengths for both scheduling modes (8 passes), so launch overhead
             // does not decide between them
@@ -3238,17 +3257,19 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         int bv = int(std::find(vars.begin(), vars.end(), def_var) - vars.begin());
         int bz = 0;
         int bc = def_c;  // the default's scheduling (auto policy: chained on small grids)
-        double bs = measure(bv, bz, bc);
+        int bt = def_s;  // the default's tile order (the auto rule)
+        double bs = measure(bv, bz, bc, bt);
         while (true) {
-            int nv2 = bv, nz2 = bz, nc2 = bc;
+            int nv2 = bv, nz2 = bz, nc2 = bc, nt2 = bt;
             double ns = bs;
-            const int cand[6][3] = {{bv - 1, bz, bc}, {bv + 1, bz, bc}, {bv, bz - 1, bc},
-                                    {bv, bz + 1, bc}, {bv, bz, bc - 1}, {bv, bz, bc + 1}};
+            const int cand[8][4] = {{bv - 1, bz, bc, bt}, {bv + 1, bz, bc, bt}, {bv, bz - 1, bc, bt},
+                                    {bv, bz + 1, bc, bt}, {bv, bz, bc - 1, bt}, {bv, bz, bc + 1, bt},
+                                    {bv, bz, bc, bt - 1}, {bv, bz, bc, bt + 1}};
             for (auto& c : cand) {
                 if (c[0] < 0 || c[0] >= int(vars.size()) || c[1] < 0 || c[1] >= nz_opts ||
-                    c[2] < 0 || c[2] >= nc_opts)
+                    c[2] < 0 || c[2] >= nc_opts || c[3] < 0 || c[3] >= ns_opts)
                     continue;
-                const double sc = measure(c[0], c[1], c[2]);
+                const double sc = measure(c[0], c[1], c[2], c[3]);
                 // move only on an improvement beyond run-to-run noise: short boost-clock
                 // measurements overstate small gains (const25pt 512^3 chained: +1% tuned,
                 // -6% in a sustained 100-step run)
@@ -3257,12 +3278,14 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
                     nv2 = c[0];
                     nz2 = c[1];
                     nc2 = c[2];
+                    nt2 = c[3];
                 }
             }
-            if (nv2 == bv && nz2 == bz && nc2 == bc) break;
+            if (nv2 == bv && nz2 == bz && nc2 == bc && nt2 == bt) break;
             bv = nv2;
             bz = nz2;
             bc = nc2;
+            bt = nt2;
             bs = ns;
         }
         // restore
@@ -3279,6 +3302,7 @@ int girih_gpu_tune(void* handle, int max_tb_req, girih_gpu_config* best, double*
         best->variant = vars[bv];
         best->zchunks = zopts[bz];
         best->chain = copts[bc];
+        best->tile_order = copts[bc] > 0 ? cfg_saved.tile_order : sopts[bt];
         if (best_mlups) *best_mlups = bs;
         if (n_measured) *n_measured = measured;
     });

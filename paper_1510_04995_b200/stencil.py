@@ -109,10 +109,12 @@ class GpuConfig:
     emulate_slabs: int = 0  # >1: that many z-slabs on ONE device (decomposition tests)
     chain: int = 0       # 1: chain same-depth passes into one dependency-driven launch; -1: off;
                          # 0: auto (grids <= 256^3 cells, not var7pt)
+    tile_order: int = 0  # W > 0: column strips of W tiles inside a z-chunk row; -1: row-major;
+                         # 0: auto (strips of 8 for var7pt two-step passes, >= 17 tile columns)
 
     def to_c(self) -> GirihGpuConfig:
         return GirihGpuConfig(self.tb, self.variant, self.zchunks, self.ngpus, 1, self.device,
-                              self.graphs, self.emulate_slabs, self.chain)
+                              self.graphs, self.emulate_slabs, self.chain, self.tile_order)
 
 
 @dataclass
@@ -440,7 +442,7 @@ class DeviceState:
         check(load().girih_gpu_tune(self._handle(), int(max_tb), C.byref(best), C.byref(mlups),
                                     C.byref(n)))
         cfg = GpuConfig(best.tb, best.variant, best.zchunks, best.ngpus, best.device, best.graphs,
-                        best.reserved, best.chain)
+                        best.reserved, best.chain, best.tile_order)
         return cfg, mlups.value, n.value
 
     def close(self) -> None:

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(girih):
 
 
 def test_abi_version(girih):
-    assert girih.load().girih_gpu_abi_version() == 5
+    assert girih.load().girih_gpu_abi_version() == 6
 
 
 def test_traits_and_names(girih):

@@ -97,6 +97,24 @@ def test_every_variant(girih, oracle, kind):
         assert_state_equal(st, ref, f"variant {v}")
 
 
+@pytest.mark.parametrize("kind", [0, 1, 2, 3], ids=KIND_IDS)
+def test_tile_order(girih, oracle, kind):
+    # GpuConfig.tile_order: column strips of W tiles inside a z-chunk row (partial last strip,
+    # W wider than the grid) and row-major give the same bits; graphs are cached per order
+    g = girih
+    base = oracle.init_state(kind, 150, 41, 17, 0, 21, remap=True)
+    ref = base.copy()
+    oracle.naive_sweep(ref, 5)
+    with g.DeviceState.from_state(to_problem(g, base), g.GpuConfig(chain=-1)) as ds:
+        for order in (-1, 2, 3, 64, 0):
+            ds.upload(to_problem(g, base))
+            ds.set_config(g.GpuConfig(chain=-1, tile_order=order))
+            ds.step(5)
+            assert_state_equal(ds.download(), ref, f"tile_order={order}")
+    with pytest.raises(g.GirihError):
+        g.run(to_problem(g, base), 1, g.GpuConfig(tile_order=-2))
+
+
 def test_narrow_variants(girih, oracle):
     # inner-columns-only tiles (ZwaveConfig::NARROW): several tiles per row with a partial last
     # one and odd extents, per-pass and chained launches, forced z chunks, emulated slabs and an

@@ -235,7 +235,7 @@ std::string tuned_key(const Options& o) {
 }
 
 bool find_tuned(const std::string& path, const std::string& key, int* tb, int* variant,
-                int* zchunks, int* chain = nullptr) {
+                int* zchunks, int* chain = nullptr, int* tile_order = nullptr) {
     std::ifstream in(path);
     std::string line;
     while (std::getline(in, line)) {
@@ -249,6 +249,7 @@ bool find_tuned(const std::string& path, const std::string& key, int* tb, int* v
         *variant = field("variant_index");
         *zchunks = field("zchunks");
         if (chain) *chain = field("chain");  // absent in older records: 0 = auto
+        if (tile_order) *tile_order = field("tile_order");  // likewise
         return true;
     }
     return false;
@@ -262,7 +263,7 @@ int cmd_run(const Options& o) {
     cfg.variant = o.variant;
     if (!o.use_tuned.empty()) {
         if (!find_tuned(o.use_tuned, tuned_key(o), &cfg.tb, &cfg.variant, &cfg.zchunks,
-                        &cfg.chain))
+                        &cfg.chain, &cfg.tile_order))
             throw std::runtime_error("no tuned configuration for this case in " + o.use_tuned +
                                      "; run `girih_gpu tune` first");
     }
@@ -346,10 +347,11 @@ int cmd_tune(const Options& o) {
     std::ofstream os(out, std::ios::app);
     os << "{\"key\":" << key << ",\"best\":{\"tb\":" << best.tb << ",\"variant_index\":"
        << best.variant << ",\"zchunks\":" << best.zchunks << ",\"chain\":" << best.chain
-       << ",\"mlups\":" << mlups
+       << ",\"tile_order\":" << best.tile_order << ",\"mlups\":" << mlups
        << ",\"measured\":" << measured << "}}\n";
     std::cout << "tuned " << key << " tb=" << best.tb << " variant=" << best.variant
-              << " zchunks=" << best.zchunks << " chain=" << best.chain << " mlups=" << mlups
+              << " zchunks=" << best.zchunks << " chain=" << best.chain
+              << " tile_order=" << best.tile_order << " mlups=" << mlups
               << '\n';
     return 0;
 }
