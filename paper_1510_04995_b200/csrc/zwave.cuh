@@ -370,6 +370,25 @@ __device__ __forceinline__ unsigned sm_id() {
     return r;
 }
 
+// stores the cells of a pair selected by m (bit 0: x at a0, bit 1: y at a1; 3: both as one
+// 16-byte store at a0) as predicated stores in straight-line code: the fused inner-columns-only
+// tile has a half-output pair in the first and last lane of every warp, and a branchy version
+// made every warp run both the vector and the scalar path
+__device__ __forceinline__ void st_pair_masked(double* a0, double* a1, double2 v, uint32_t m) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p1, p2, p3;\n"
+        "setp.eq.u32 p3, %4, 3;\n"
+        "setp.eq.u32 p1, %4, 1;\n"
+        "setp.eq.u32 p2, %4, 2;\n"
+        "@p3 st.global.v2.f64 [%0], {%2, %3};\n"
+        "@p1 st.global.f64 [%0], %2;\n"
+        "@p2 st.global.f64 [%1], %3;\n"
+        "}\n" ::"l"(a0),
+        "l"(a1), "d"(v.x), "d"(v.y), "r"(m)
+        : "memory");
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -1366,7 +1385,16 @@ __global__ void __launch_bounds__(NT, (CHAIN && GIRIH_CHAIN_MINB_DROP && MINB > 
                         // 16-byte store (x pair origins are even, off + R is even)
                         double* dst = (CHAIN ? SU2[seq & 1].dst_final : p.dst_final) + (long long)k * p.plane;
                         constexpr uint32_t FULL = PPT == 16 ? 0xffffffffu : (1u << (2 * PPT)) - 1u;
-                        if (dmask == FULL) {  // every pair whole (all threads of interior tiles)
+                        if constexpr (!(NARROW && TB == 1) && PPT == 1) {
+                            // (edge lanes of every warp hold halo or half-output pairs: no
+                            // per-thread fast path, which would make every warp run both paths;
+                            // measured: var7pt 1024^3 +2.7%, 384^3 +2.4%, 512^3 +1.0%; two-pair
+                            // const7pt threads 512^3 -0.9%, so those keep the branch)
+#pragma unroll
+                            for (int i = 0; i < PPT; ++i)
+                                st_pair_masked(dst + colidx[2 * i], dst + colidx[2 * i + 1], val[i],
+                                               (dmask >> (2 * i)) & 3u);
+                        } else if (dmask == FULL) {  // every pair whole (all threads of interior tiles)
                             if constexpr (CFG::STACK) {
                                 // a thread's pairs sit in consecutive rows of one column (no
                                 // clamped coordinate in a whole-pair thread): one base, row pitch
